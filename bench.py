@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""bench.py — lower bounds/sec on Taillard 200x20 pools (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config ta091] [--pool NODES_PER_GPU] [--no-e2e] [--no-bb]
+
+One step = one fsp_lb_eval over the whole per-GPU pool (every row a1-a5 of
+SURVEY.md §8(a) runs inside the kernel), pool resident in HBM.  Under torchrun
+each rank bounds its own pool (weak scaling, no data-path collective); the
+reported time is the max over ranks.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_1208_3933_b200 import inputs  # noqa: E402
+
+METRIC = "lower bounds/sec on Taillard 200x20 pools"
+UNIT = "bounds/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="ta091")
+    ap.add_argument("--pool", type=int, default=1 << 20)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-bb", action="store_true")
+    ap.add_argument("--bb-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(cfg, pool, world):
+    n, m, seed = inputs.TAILLARD_SEEDS[cfg]
+    return {
+        "workload": f"{cfg}-class {n}x{m} tai-gen(seed {seed}), D1 pool {pool} nodes/GPU",
+        "instance": cfg, "n": n, "m": m, "pool_per_gpu": pool, "total_pool": pool * world,
+        "stride": inputs.default_stride(n), "pool_recipe": "D1 (DESIGN.md §5)",
+        "l2": "inputs exceed L2 (prefix pool > 126 MB), no flush needed"
+        if pool * inputs.default_stride(n) * 2 > 126e6 else "pool fits L2: L2 flushed between steps",
+        "parallelism": f"pool-sharded x{world}",
+    }
+
+
+def algorithmic_ops(n, m, depth):
+    """Sum over the pool of W(d) (= fsp_lb_work per node)."""
+    P = m * (m - 1) // 2
+    d = depth.astype(np.int64)
+    npr = n - d
+    return int((2 * d * m + npr * (3 * m - 2) + npr * m + P * n + 4 * P * npr + 2 * P).sum())
+
+
+def alu_peak_tops():
+    """Integer issue peak: 148 SMs x 4 SMSPs x 32 lanes x 1 warp-instr/clk at
+    the max SM clock (clock from MEASURED_PEAKS.json)."""
+    mhz = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", mhz))
+    except Exception:
+        pass
+    return 148 * 4 * 32 * mhz * 1e6 / 1e12, mhz
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for nm, v in zip(names, r[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ncu_traffic(cfg):
+    """dram read+write bytes per launch of the lb kernel from the committed
+    ncu --set full summary (profiles/), if one exists for this workload."""
+    p = os.path.join(ROOT, "profiles", "lb_kernel_ncu.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        if d.get("instance") == cfg:
+            return d.get("dram_bytes_per_launch"), d
+    except Exception:
+        pass
+    return None, None
+
+
+def cpu_oracle_rate(ptm, pf, dp, seconds, threads=None):
+    """The oracle as it stands on the host cores: contiguous chunks of a
+    bounded sample, one ctypes call per thread (the C code releases the GIL)."""
+    import oracle
+    T = oracle.Tables(ptm)
+    threads = threads or len(os.sched_getaffinity(0))
+    # size the sample from a 1-thread probe
+    probe = min(len(dp), 64)
+    t0 = time.perf_counter()
+    T.lb_eval(pf[:probe], dp[:probe])
+    per_node = (time.perf_counter() - t0) / probe
+    S = int(min(len(dp), max(threads * 8, seconds * threads / max(per_node, 1e-9))))
+    chunks = np.array_split(np.arange(S), threads)
+    res = [None] * threads
+
+    def work(i):
+        idx = chunks[i]
+        res[i] = T.lb_eval(pf[idx[0]:idx[-1] + 1], dp[idx[0]:idx[-1] + 1]) if len(idx) else None
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    dt = time.perf_counter() - t0
+    return S / dt, threads, S, dt
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = a.config
+    n, m, seed = inputs.TAILLARD_SEEDS[cfg]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, min(a.pool, 200_000), inputs.pool_seed(cfg))
+    import oracle
+    T = oracle.Tables(ptm)
+    threads = len(os.sched_getaffinity(0))
+    # per-step sample: ~4 s of CPU work on all cores
+    rate_probe, _, _, _ = cpu_oracle_rate(ptm, pf, dp, 1.0, threads)
+    S = int(max(threads, min(len(dp), rate_probe * 4.0)))
+    chunks = np.array_split(np.arange(S), threads)
+
+    def step():
+        def work(i):
+            idx = chunks[i]
+            if len(idx):
+                T.lb_eval(pf[idx[0]:idx[-1] + 1], dp[idx[0]:idx[-1] + 1])
+        ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+
+    for _ in range(a.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = S * a.steps / dt
+    cfgd = workload(cfg, a.pool, world)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt / a.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": cfgd,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"first {S} nodes of the D1 pool per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1208_3933_b200 import binding
+
+    rank, world, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = a.config
+    n, m, seed = inputs.TAILLARD_SEEDS[cfg]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, a.pool, inputs.pool_seed(cfg) + 1000 * rank)
+    stride = pf.shape[1]
+    inst = binding.Instance(ptm)
+    d_pf = torch.from_numpy(pf.view(np.int16)).cuda()
+    d_dp = torch.from_numpy(dp).cuda()
+    d_lb = torch.empty(a.pool, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(a.warmup, 3)):
+        inst.lb_eval(d_pf, d_dp, out=d_lb, stream=stream)
+    torch.cuda.synchronize()
+    if inst.check() != binding.FSP_OK:
+        raise SystemExit("malformed node in bench pool")
+
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(a.steps):
+            inst.lb_eval(d_pf, d_dp, out=d_lb, stream=stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = a.pool * world * a.steps / (ms_max / 1e3)
+
+    # roofline: algorithmic integer ops per launch / mean launch time
+    ops = algorithmic_ops(n, m, dp)
+    peak, mhz = alu_peak_tops()
+    achieved = ops / (ms / a.steps / 1e3) / 1e12
+    traffic, _ = ncu_traffic(cfg)
+
+    # e2e through the C ABI with pinned HOST buffers (copies inside the timed region)
+    e2e = None
+    if not a.no_e2e:
+        h_pf = torch.from_numpy(pf.view(np.int16)).pin_memory()
+        h_dp = torch.from_numpy(dp).pin_memory()
+        h_lb = torch.empty(a.pool, dtype=torch.int32).pin_memory()
+        inst.lb_eval_host_ptr(h_pf.data_ptr(), stride, h_dp.data_ptr(), a.pool, h_lb.data_ptr())
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            inst.lb_eval_host_ptr(h_pf.data_ptr(), stride, h_dp.data_ptr(), a.pool,
+                                  h_lb.data_ptr())
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        if not torch.equal(h_lb, d_lb.cpu()):
+            raise SystemExit("host-API LBs differ from device LBs")
+        e2e = {"value": a.pool * world * a.steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": int(pf.nbytes + dp.nbytes),
+               "d2h_bytes_per_step": int(a.pool * 4)}
+
+    bb = None
+    if not a.no_bb and rank == 0:
+        try:
+            rc, msp, perm, st = inst.bb_solve(2**31 - 1, 0, a.bb_seconds)
+            bb = {"bounded_nodes_per_s": st["bounded"] / max(st["wall_s"], 1e-9),
+                  "status": int(rc), "incumbent": msp, "wall_s": st["wall_s"], **st}
+        except Exception as ex:  # B&B is reported beside the metric, never instead of it
+            bb = {"error": str(ex)[:200]}
+
+    cpu = None
+    if rank == 0:
+        rate, cores, S, dt = cpu_oracle_rate(ptm, pf, dp, a.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"first {S} nodes of the rank-0 D1 pool ({dt:.1f} s on {cores} threads)"}
+
+    if rank == 0:
+        cfgd = workload(cfg, a.pool, world)
+        info = inst.info
+        cfgd["lb_kernel"] = {k: info[k] for k in ("groups", "pairs_per_group", "warps_per_cta",
+                                                  "ctas_per_sm", "smem_bytes", "maxm")}
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": max(a.warmup, 3), "ms_per_step": ms_max / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": cfgd,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Top/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_note": f"int issue peak 148 SM x 128 lanes x {mhz:.0f} MHz "
+                                      "(DESIGN.md §7)",
+                         "ops_per_launch": ops},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": a.steps,
+            "clocks": clk.summary(), "bb": bb,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

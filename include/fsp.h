@@ -1,0 +1,179 @@
+/*
+ * fsp.h — C ABI of libfsp.so, the B200 (sm_100a) hot path of
+ * Melab, Chakroun, Mezmaz, Tuyttens, "A GPU-accelerated Branch-and-Bound
+ * Algorithm for the Flow-Shop Scheduling Problem", arXiv 1208.3933.
+ *
+ * Citations "P:a-b" are lines of the paper's LaTeX source.
+ * Readings R1..R18 of silent or garbled passages are listed in DESIGN.md §3.
+ *
+ * Conventions for every entry point:
+ *  - Return value: int status, FSP_OK (0) or a negative FSP_E* code; the
+ *    message of the last failure on the calling thread is fsp_last_error().
+ *  - "DEVICE" pointers are CUDA global-memory pointers on the device that was
+ *    current when the instance was loaded (one process per GPU); "HOST"
+ *    pointers are ordinary (optionally pinned) host memory.
+ *  - Nothing here takes ownership of caller memory; outputs are written,
+ *    inputs are only read.
+ *  - cuda_stream is a cudaStream_t (NULL = legacy default stream).  Calls that
+ *    take a stream are stream-ordered and asynchronous; they allocate nothing
+ *    and never synchronise the host.
+ */
+#ifndef FSP_H
+#define FSP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    FSP_OK = 0,
+    FSP_EINVAL = -1,    /* null pointer, bad size, bad argument            */
+    FSP_ERANGE = -2,    /* instance outside the supported value ranges     */
+    FSP_ENOMEM = -3,    /* host or device allocation failed                */
+    FSP_ECUDA = -4,     /* a CUDA runtime call failed                      */
+    FSP_ENOTFOUND = -5, /* B&B: no schedule with makespan <= initial_ub    */
+    FSP_EBUDGET = -6,   /* B&B: node/time budget exhausted before proof    */
+    FSP_EBADNODE = -7   /* a malformed node was seen by a batched call     */
+};
+
+#define FSP_MAX_JOBS 4096
+#define FSP_MAX_MACHINES 32
+
+typedef struct fsp_instance fsp_instance; /* opaque, immutable after load */
+
+/* ------------------------------------------------------------------ instance
+ * fsp_instance_load — the problem statement of §II-B: n jobs,
+ * m machines, processing times p_{j,k}.  Builds, on the host, the per-couple
+ * structures of §II-D: the couples MM (k<l), and for
+ * each couple the Johnson-with-lags order JM (R7/R8) with each
+ * job's lag folded into two per-(couple, position) constants,
+ * then uploads them once to the current device (the paper's "computed once
+ * at the beginning").
+ *   ptm     HOST, row-major [n_jobs][n_machines], ptm[j*m + k] = p_{j,k}
+ *           (job-major as Fig. 3's PTM[job][M], R16).  Copied.
+ *   out     receives the instance handle; free with fsp_instance_free.
+ * Errors: EINVAL (null, n < 1, m < 2, any p < 0); ERANGE (n > FSP_MAX_JOBS,
+ * m > FSP_MAX_MACHINES, max p > 32767, or (n+m-1)*max p >= 2^31, R12);
+ * ENOMEM / ECUDA. */
+int fsp_instance_load(const int32_t *ptm, int32_t n_jobs, int32_t n_machines,
+                      fsp_instance **out);
+void fsp_instance_free(fsp_instance *inst);
+
+typedef struct {
+    int32_t n, m, P;          /* jobs, machines, couples m(m-1)/2          */
+    int32_t device;           /* CUDA ordinal the tables live on           */
+    int32_t groups;           /* couple groups staged into shared memory   */
+    int32_t pairs_per_group;
+    int32_t warps_per_cta;    /* lb kernel launch shape                    */
+    int32_t ctas_per_sm;
+    int32_t smem_bytes;       /* dynamic shared memory per CTA             */
+    int32_t maxm;             /* machine-count specialisation used         */
+    int64_t table_bytes;      /* device bytes of the couple tables         */
+} fsp_instance_info;
+
+int fsp_instance_get_info(const fsp_instance *inst, fsp_instance_info *info);
+
+/* ------------------------------------------------------------------- bounding
+ * fsp_lb_eval — the bounding operator of §III-A applied to a pool of
+ * sub-problems: lb_out[i] = LB of node i, the lower bound of
+ * Fig. 3 with the readings R1-R6.
+ *   prefix  DEVICE uint16 [pool][stride]; node i is the partial schedule
+ *           pi(1..d) = prefix[i*stride .. i*stride + depth[i]).
+ *           Entries past depth[i] are not read.  stride >= 1.
+ *   depth   DEVICE int32 [pool], 0 <= depth[i] <= n.  depth == n returns the
+ *           makespan (R6); depth == n-1 returns the exact makespan of the
+ *           forced completion.
+ *   lb_out  DEVICE int32 [pool]; each element written exactly once and
+ *           depending only on node i (order-preserving, pure).
+ *   pool    number of nodes, >= 0 (0 is a no-op).
+ * Malformed nodes (job >= n, repeated job, depth outside [0,n]) never cause
+ * an out-of-bounds access: their LB is unspecified and a device flag is set,
+ * reported as FSP_EBADNODE by fsp_check.  Errors: EINVAL, ECUDA (launch). */
+int fsp_lb_eval(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
+                const int32_t *depth, int64_t pool, int32_t *lb_out, void *cuda_stream);
+
+/* fsp_lb_eval_host — same result with HOST buffers (the paper's offload
+ * round trip): copies the pool to the device in chunks, bounds each
+ * chunk and copies the LBs back, overlapping the three on two streams.
+ * Synchronous: returns when lb_out is filled.  Pinned host memory gives full
+ * PCIe bandwidth; pageable memory works but slower.  Returns FSP_EBADNODE if
+ * a malformed node was seen.  Errors: EINVAL, ENOMEM, ECUDA. */
+int fsp_lb_eval_host(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
+                     const int32_t *depth, int64_t pool, int32_t *lb_out);
+
+/* fsp_check — synchronises cuda_stream, then returns FSP_EBADNODE (and clears
+ * the flag) if any bounding call on this instance saw a malformed node since
+ * the last check, else FSP_OK. */
+int fsp_check(const fsp_instance *inst, void *cuda_stream);
+
+/* fsp_lb_work — algorithmic integer operations of Fig. 3 for one node of
+ * depth d (the roofline numerator):
+ *   W(d) = 2dm + n'(3m-2) + n'm + P*n + 4*P*n' + 2P,  n' = n - d. */
+int64_t fsp_lb_work(int32_t n, int32_t m, int32_t d);
+
+/* ------------------------------------------------------------------ B&B
+ * fsp_bb_solve — the B&B of §II-A/§II-B with the
+ * bounding, elimination and branching operators all on the device (pool never
+ * round-trips through the host per iteration).  Returns a permutation with the
+ * minimal makespan among those with makespan <= initial_ub
+ * (INT32_MAX = unbounded); elimination prunes LB >= incumbent with the
+ * incumbent started at initial_ub + 1 (R9).
+ *   makespan_out  HOST int32: the optimum (or the incumbent on EBUDGET).
+ *   perm_out      HOST int32 [n]: a schedule attaining it.
+ *   stats         HOST, nullable.
+ *   max_nodes     budget on bounded nodes (<= 0: none); time_limit_s
+ *                 (<= 0: none).  On budget exhaustion returns FSP_EBUDGET
+ *                 with the incumbent (not proven optimal), or FSP_ENOTFOUND
+ *                 if none was found.
+ * Errors: EINVAL, ENOMEM, ECUDA, ENOTFOUND, EBUDGET. */
+typedef struct {
+    int64_t bounded;      /* child lower bounds evaluated                  */
+    int64_t branched;     /* parents decomposed                            */
+    int64_t pruned;       /* children eliminated (LB >= incumbent)         */
+    int64_t leaves;       /* complete schedules evaluated                  */
+    int64_t iterations;   /* device expand/bound/prune steps               */
+    double wall_s;        /* host wall time of the solve                   */
+} fsp_bb_stats;
+
+int fsp_bb_solve(const fsp_instance *inst, int32_t initial_ub, int64_t max_nodes,
+                 double time_limit_s, int32_t *makespan_out, int32_t *perm_out,
+                 fsp_bb_stats *stats);
+
+/* Step-level B&B for the multi-GPU driver (torch.distributed owns the
+ * collectives).  A state holds one device-resident pool.
+ *  fsp_bb_init        state for rank/world (rank r keeps the root's
+ *                     descendants assigned to it).
+ *  fsp_bb_step        up to `iters` expand/bound/prune iterations on stream;
+ *                     synchronous (reads the pool size back).
+ *  fsp_bb_ub_ptr      DEVICE int64 word = (incumbent << 32) | rank, for a
+ *                     MIN all-reduce; after the collective call
+ *                     fsp_bb_ub_sync to adopt the global incumbent.
+ *  fsp_bb_pool_size   HOST out: open nodes in the pool.
+ *  fsp_bb_export      move up to max_nodes open nodes into a DEVICE buffer of
+ *                     fsp_bb_node_bytes(state) bytes per node (donor side).
+ *  fsp_bb_import      append n nodes from such a DEVICE buffer (receiver).
+ *  fsp_bb_result      incumbent and its permutation (HOST), FSP_ENOTFOUND if
+ *                     this rank holds none.
+ *  fsp_bb_get_stats   counters of this rank. */
+int fsp_bb_init(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_t world,
+                void **state);
+int fsp_bb_step(void *state, int32_t iters, void *cuda_stream);
+int fsp_bb_ub_ptr(void *state, int64_t **d_packed_ub);
+int fsp_bb_ub_sync(void *state, void *cuda_stream);
+int fsp_bb_pool_size(void *state, int64_t *n);
+int64_t fsp_bb_node_bytes(void *state);
+int fsp_bb_export(void *state, int64_t max_nodes, void *d_buf, int64_t *n_out);
+int fsp_bb_import(void *state, const void *d_buf, int64_t n);
+int fsp_bb_result(void *state, int32_t *makespan_out, int32_t *perm_out);
+int fsp_bb_get_stats(void *state, fsp_bb_stats *stats);
+void fsp_bb_free(void *state);
+
+const char *fsp_last_error(void); /* thread-local; never NULL */
+int fsp_version(void);            /* ABI version, currently 1 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSP_H */

@@ -1,0 +1,190 @@
+"""Thin ctypes binding of libfsp.so (include/fsp.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  Device buffers are torch CUDA tensors (PyTorch supplies memory
+and streams); host buffers are numpy arrays.  There is no CPU fallback: if the
+library is missing or fails to load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfsp.so")
+
+FSP_OK, FSP_EINVAL, FSP_ERANGE, FSP_ENOMEM, FSP_ECUDA = 0, -1, -2, -3, -4
+FSP_ENOTFOUND, FSP_EBUDGET, FSP_EBADNODE = -5, -6, -7
+_NAMES = {0: "FSP_OK", -1: "FSP_EINVAL", -2: "FSP_ERANGE", -3: "FSP_ENOMEM", -4: "FSP_ECUDA",
+          -5: "FSP_ENOTFOUND", -6: "FSP_EBUDGET", -7: "FSP_EBADNODE"}
+
+# every symbol include/fsp.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "fsp_instance_load", "fsp_instance_free", "fsp_instance_get_info", "fsp_lb_eval",
+    "fsp_lb_eval_host", "fsp_check", "fsp_lb_work", "fsp_bb_solve", "fsp_bb_init",
+    "fsp_bb_step", "fsp_bb_ub_ptr", "fsp_bb_ub_sync", "fsp_bb_pool_size", "fsp_bb_node_bytes",
+    "fsp_bb_export", "fsp_bb_import", "fsp_bb_result", "fsp_bb_get_stats", "fsp_bb_free",
+    "fsp_last_error", "fsp_version",
+]
+
+
+class FspError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class InstanceInfo(C.Structure):
+    _fields_ = [("n", C.c_int32), ("m", C.c_int32), ("P", C.c_int32), ("device", C.c_int32),
+                ("groups", C.c_int32), ("pairs_per_group", C.c_int32),
+                ("warps_per_cta", C.c_int32), ("ctas_per_sm", C.c_int32),
+                ("smem_bytes", C.c_int32), ("maxm", C.c_int32), ("table_bytes", C.c_int64)]
+
+
+class BBStats(C.Structure):
+    _fields_ = [("bounded", C.c_int64), ("branched", C.c_int64), ("pruned", C.c_int64),
+                ("leaves", C.c_int64), ("iterations", C.c_int64), ("wall_s", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libfsp.so (raises if absent: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        sig = {
+            "fsp_instance_load": (C.c_int, [vp, i32, i32, C.POINTER(vp)]),
+            "fsp_instance_free": (None, [vp]),
+            "fsp_instance_get_info": (C.c_int, [vp, C.POINTER(InstanceInfo)]),
+            "fsp_lb_eval": (C.c_int, [vp, vp, i32, vp, i64, vp, vp]),
+            "fsp_lb_eval_host": (C.c_int, [vp, vp, i32, vp, i64, vp]),
+            "fsp_check": (C.c_int, [vp, vp]),
+            "fsp_lb_work": (i64, [i32, i32, i32]),
+            "fsp_bb_solve": (C.c_int, [vp, i32, i64, C.c_double, C.POINTER(i32), vp,
+                                       C.POINTER(BBStats)]),
+            "fsp_bb_init": (C.c_int, [vp, i32, i32, i32, C.POINTER(vp)]),
+            "fsp_bb_step": (C.c_int, [vp, i32, vp]),
+            "fsp_bb_ub_ptr": (C.c_int, [vp, C.POINTER(vp)]),
+            "fsp_bb_ub_sync": (C.c_int, [vp, vp]),
+            "fsp_bb_pool_size": (C.c_int, [vp, C.POINTER(i64)]),
+            "fsp_bb_node_bytes": (i64, [vp]),
+            "fsp_bb_export": (C.c_int, [vp, i64, vp, C.POINTER(i64)]),
+            "fsp_bb_import": (C.c_int, [vp, vp, i64]),
+            "fsp_bb_result": (C.c_int, [vp, C.POINTER(i32), vp]),
+            "fsp_bb_get_stats": (C.c_int, [vp, C.POINTER(BBStats)]),
+            "fsp_bb_free": (None, [vp]),
+            "fsp_last_error": (C.c_char_p, []),
+            "fsp_version": (C.c_int, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc, allow=()):
+    if rc != FSP_OK and rc not in allow:
+        raise FspError(rc, lib().fsp_last_error().decode())
+    return rc
+
+
+def _ptr(t):
+    """Device pointer of a torch tensor (must be contiguous CUDA)."""
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("expected a contiguous CUDA tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def fsp_lb_work(n: int, m: int, d: int) -> int:
+    return int(lib().fsp_lb_work(n, m, d))
+
+
+class Instance:
+    """An fsp_instance (tables resident on the current CUDA device)."""
+
+    def __init__(self, ptm):
+        ptm = np.ascontiguousarray(ptm, dtype=np.int32)
+        if ptm.ndim != 2:
+            raise ValueError("ptm must be [n][m]")
+        self.n, self.m = ptm.shape
+        self.ptm = ptm
+        h = C.c_void_p()
+        _check(lib().fsp_instance_load(ptm.ctypes.data, self.n, self.m, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().fsp_instance_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def info(self) -> dict:
+        inf = InstanceInfo()
+        _check(lib().fsp_instance_get_info(self._h, C.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in InstanceInfo._fields_}
+
+    def lb_eval(self, prefix, depth, out=None, stream=None):
+        """fsp_lb_eval on torch CUDA tensors: prefix uint16-compatible
+        [pool][stride] (torch.int16 storage), depth int32 [pool]."""
+        import torch
+        pool = depth.shape[0]
+        if out is None:
+            out = torch.empty(pool, dtype=torch.int32, device=depth.device)
+        stride = prefix.shape[1] if prefix.dim() == 2 else 1
+        _check(lib().fsp_lb_eval(self._h, _ptr(prefix), stride, _ptr(depth), pool, _ptr(out),
+                                 _stream(stream)))
+        return out
+
+    def lb_eval_host(self, prefix: np.ndarray, depth: np.ndarray, out=None):
+        """fsp_lb_eval_host on numpy arrays (host memory, synchronous)."""
+        prefix = np.ascontiguousarray(prefix, dtype=np.uint16)
+        depth = np.ascontiguousarray(depth, dtype=np.int32)
+        pool = depth.shape[0]
+        if out is None:
+            out = np.empty(pool, np.int32)
+        stride = prefix.shape[1] if prefix.ndim == 2 else 1
+        _check(lib().fsp_lb_eval_host(self._h, prefix.ctypes.data, stride, depth.ctypes.data,
+                                      pool, out.ctypes.data))
+        return out
+
+    def lb_eval_host_ptr(self, prefix_ptr: int, stride: int, depth_ptr: int, pool: int,
+                         out_ptr: int):
+        """fsp_lb_eval_host on raw host pointers (e.g. pinned torch tensors)."""
+        _check(lib().fsp_lb_eval_host(self._h, C.c_void_p(prefix_ptr), stride,
+                                      C.c_void_p(depth_ptr), pool, C.c_void_p(out_ptr)))
+
+    def check(self, stream=None) -> int:
+        """fsp_check: FSP_OK or FSP_EBADNODE (raises on other errors)."""
+        return _check(lib().fsp_check(self._h, _stream(stream)), allow=(FSP_EBADNODE,))
+
+    def bb_solve(self, initial_ub: int = 2**31 - 1, max_nodes: int = 0, time_limit_s: float = 0.0):
+        """fsp_bb_solve.  Returns (status, makespan, perm, stats)."""
+        ms = C.c_int32(0)
+        perm = np.zeros(self.n, np.int32)
+        st = BBStats()
+        rc = lib().fsp_bb_solve(self._h, int(initial_ub), int(max_nodes), float(time_limit_s),
+                                C.byref(ms), perm.ctypes.data, C.byref(st))
+        _check(rc, allow=(FSP_ENOTFOUND, FSP_EBUDGET))
+        return rc, int(ms.value), perm, {f: getattr(st, f) for f, _ in BBStats._fields_}

@@ -1,0 +1,164 @@
+// instance.cu — fsp_instance_load: host precompute of the per-couple tables
+// (§II-D) and their one-time upload.
+//
+// Independent of oracle/: the couples, lags and Johnson orders are rebuilt
+// here from row prefix sums, and only the two walk constants per (couple,
+// position) are kept:
+//   S_j[x] = sum_{i<x} p_{j,i}
+//   a_j  = p_{j,k} + lag_j(k,l) = S_j[l]   - S_j[k]      (Johnson key, machine 1)
+//   b_j  = lag_j(k,l) + p_{j,l} = S_j[l+1] - S_j[k+1]    (Johnson key, machine 2)
+//   c1_j = a_j,   c2_j = p_{j,k} - p_{j,l}
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <numeric>
+#include <vector>
+
+#include "fsp_internal.h"
+
+static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_instance **out)
+{
+    if (!ptm || !out) return fsp_fail(FSP_EINVAL, "null pointer");
+    *out = nullptr;
+    if (n < 1 || m < 2) return fsp_fail(FSP_EINVAL, "need n >= 1 and m >= 2");
+    if (n > FSP_MAX_JOBS) return fsp_fail(FSP_ERANGE, "n > FSP_MAX_JOBS");
+    if (m > FSP_MAX_MACHINES) return fsp_fail(FSP_ERANGE, "m > FSP_MAX_MACHINES");
+    int64_t maxp = 0;
+    for (int64_t i = 0; i < (int64_t)n * m; ++i) {
+        if (ptm[i] < 0) return fsp_fail(FSP_EINVAL, "negative processing time");
+        maxp = std::max<int64_t>(maxp, ptm[i]);
+    }
+    if (maxp > 32767) return fsp_fail(FSP_ERANGE, "processing time > 32767");
+    if ((int64_t)(n + m - 1) * maxp >= INT32_MAX)
+        return fsp_fail(FSP_ERANGE, "(n+m-1)*max p overflows int32");
+
+    fsp_instance *inst = new (std::nothrow) fsp_instance();
+    if (!inst) return fsp_fail(FSP_ENOMEM, "host allocation");
+    inst->n = n;
+    inst->m = m;
+    inst->P = m * (m - 1) / 2;
+    inst->max_p = (int)maxp;
+    cudaError_t e = cudaGetDevice(&inst->device);
+    if (e != cudaSuccess) {
+        delete inst;
+        return fsp_cuda_fail(e, "cudaGetDevice");
+    }
+    inst->h_ptm = new (std::nothrow) int32_t[(size_t)n * m];
+    if (!inst->h_ptm) {
+        delete inst;
+        return fsp_fail(FSP_ENOMEM, "host allocation");
+    }
+    std::memcpy(inst->h_ptm, ptm, sizeof(int32_t) * (size_t)n * m);
+
+    int rc = fsp_plan_lb(inst);
+    if (rc != FSP_OK) {
+        fsp_instance_free(inst);
+        return rc;
+    }
+    const fsp_lb_plan &pl = inst->plan;
+    const int P = inst->P;
+
+    // ---- couple tables, grouped: [u32 (k | l<<16) x ppg][fsp_rec x np x n] ----
+    std::vector<int32_t> S((size_t)n * (m + 1));
+    for (int j = 0; j < n; ++j) {
+        S[(size_t)j * (m + 1)] = 0;
+        for (int i = 0; i < m; ++i)
+            S[(size_t)j * (m + 1) + i + 1] = S[(size_t)j * (m + 1) + i] + ptm[(size_t)j * m + i];
+    }
+    const size_t gbytes = pl.group_bytes;
+    const size_t kl_bytes = align16((size_t)pl.pairs_per_group * 4);
+    std::vector<uint8_t> blob(gbytes * pl.groups, 0);
+    std::vector<int> order(n), A(n), B(n);
+    int p = 0;
+    for (int k = 0; k < m; ++k) {
+        for (int l = k + 1; l < m; ++l, ++p) {
+            const int g = p / pl.pairs_per_group, pl_idx = p % pl.pairs_per_group;
+            uint8_t *gb = blob.data() + (size_t)g * gbytes;
+            reinterpret_cast<uint32_t *>(gb)[pl_idx] = (uint32_t)k | ((uint32_t)l << 16);
+            for (int j = 0; j < n; ++j) {
+                const int32_t *Sj = &S[(size_t)j * (m + 1)];
+                A[j] = Sj[l] - Sj[k];
+                B[j] = Sj[l + 1] - Sj[k + 1];
+            }
+            // Johnson's rule on (A, B) ("with lags" P:188-190):
+            // A <= B first by ascending A, then descending B; ties by job id.
+            std::iota(order.begin(), order.end(), 0);
+            std::sort(order.begin(), order.end(), [&](int x, int y) {
+                const bool fx = A[x] <= B[x], fy = A[y] <= B[y];
+                if (fx != fy) return fx;
+                if (fx ? A[x] != A[y] : B[x] != B[y]) return fx ? A[x] < A[y] : B[x] > B[y];
+                return x < y;
+            });
+            fsp_rec *rec = reinterpret_cast<fsp_rec *>(gb + kl_bytes) + (size_t)pl_idx * n;
+            for (int i = 0; i < n; ++i) {
+                const int j = order[i];
+                const int c2 = ptm[(size_t)j * m + k] - ptm[(size_t)j * m + l];
+                rec[i].c1 = A[j];
+                rec[i].meta = (int32_t)(((uint32_t)c2 << 16) | (uint32_t)(4 * j));
+            }
+        }
+    }
+    (void)P;
+
+    // ---- PTM as u16 rows (stride mp, even) for shared memory; int32 copy ----
+    const int mp = (m + 1) & ~1;
+    std::vector<uint16_t> p16(pl.ptm_bytes / 2, 0);
+    for (int j = 0; j < n; ++j)
+        for (int k = 0; k < m; ++k) p16[(size_t)j * mp + k] = (uint16_t)ptm[(size_t)j * m + k];
+
+    inst->table_bytes = (int64_t)blob.size();
+    e = cudaMalloc(&inst->d_tables, blob.size());
+    if (e == cudaSuccess) e = cudaMalloc(&inst->d_ptm16, pl.ptm_bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&inst->d_ptm32, sizeof(int32_t) * (size_t)n * m);
+    if (e == cudaSuccess) e = cudaMalloc(&inst->d_err, sizeof(int));
+    if (e == cudaSuccess)
+        e = cudaMemcpy(inst->d_tables, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(inst->d_ptm16, p16.data(), pl.ptm_bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(inst->d_ptm32, ptm, sizeof(int32_t) * (size_t)n * m, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(inst->d_err, 0, sizeof(int));
+    if (e != cudaSuccess) {
+        fsp_instance_free(inst);
+        return fsp_cuda_fail(e, "instance upload");
+    }
+    *out = inst;
+    return FSP_OK;
+}
+
+void fsp_host_ctx_free(void *ctx);
+
+extern "C" void fsp_instance_free(fsp_instance *inst)
+{
+    if (!inst) return;
+    if (inst->host_ctx) fsp_host_ctx_free(inst->host_ctx);
+    if (inst->d_tables) cudaFree(inst->d_tables);
+    if (inst->d_ptm16) cudaFree(inst->d_ptm16);
+    if (inst->d_ptm32) cudaFree(inst->d_ptm32);
+    if (inst->d_err) cudaFree(inst->d_err);
+    delete[] inst->h_ptm;
+    delete inst;
+}
+
+extern "C" int fsp_instance_get_info(const fsp_instance *inst, fsp_instance_info *info)
+{
+    if (!inst || !info) return fsp_fail(FSP_EINVAL, "null pointer");
+    const fsp_lb_plan &pl = inst->plan;
+    info->n = inst->n;
+    info->m = inst->m;
+    info->P = inst->P;
+    info->device = inst->device;
+    info->groups = pl.groups;
+    info->pairs_per_group = pl.pairs_per_group;
+    info->warps_per_cta = pl.warps;
+    info->ctas_per_sm = pl.ctas_per_sm;
+    info->smem_bytes = (int32_t)pl.smem_bytes;
+    info->maxm = pl.maxm;
+    info->table_bytes = inst->table_bytes;
+    return FSP_OK;
+}

@@ -1,0 +1,171 @@
+"""GPU parity: fsp_lb_eval (CUDA, through the C ABI) vs the CPU oracle.
+
+Bit-exact (integer work, tolerance 0, BASELINE.json north_star) on every node
+of seeded pools sized so the oracle finishes in seconds, plus sampled nodes of
+the full-size 200x20 pool in the launch configuration bench.py times, plus the
+edge cases (empty, ragged, d = 0 / n-1 / n, duplicates, degenerate instances,
+malformed nodes).
+"""
+import numpy as np
+import pytest
+
+from paper_1208_3933_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def fsp():
+    from paper_1208_3933_b200 import binding
+    binding.lib()
+    return binding
+
+
+def dev(torch, a):
+    if a.dtype == np.uint16:
+        a = a.view(np.int16)
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_lb(torch, inst, pf, dp):
+    out = inst.lb_eval(dev(torch, pf), dev(torch, dp))
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def compare(torch, fsp, orc, ptm, pf, dp):
+    inst = fsp.Instance(ptm)
+    got = gpu_lb(torch, inst, pf, dp)
+    assert inst.check() == fsp.FSP_OK
+    want = orc.Tables(ptm).lb_eval(pf, dp)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first {bad[:5]}: got {got[bad[:5]]} want {want[bad[:5]]}"
+    return inst
+
+
+@pytest.mark.parametrize("name,N", [("ta001", 20000), ("ta021", 65536), ("ta051", 16411),
+                                    ("ta091", 4133), ("ta111", 1061)])
+def test_parity_config_pools(torch, fsp, orc, name, N):
+    n, m, seed = inputs.TAILLARD_SEEDS[name]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, N, inputs.pool_seed(name))
+    compare(torch, fsp, orc, ptm, pf, dp)
+
+
+@pytest.mark.parametrize("d", ["zero", "n-1", "n"])
+def test_parity_fixed_depths(torch, fsp, orc, d):
+    for name in ("ta021", "ta091"):
+        n, m, seed = inputs.TAILLARD_SEEDS[name]
+        depth = {"zero": 0, "n-1": n - 1, "n": n}[d]
+        pf, dp = inputs.pool_fixed_depth(n, 300, depth, 5)
+        compare(torch, fsp, orc, inputs.taillard(n, m, seed), pf, dp)
+
+
+@pytest.mark.parametrize("m", [2, 3, 7, 11, 13, 17, 25, 32])
+def test_parity_machine_counts(torch, fsp, orc, m):
+    rng = np.random.default_rng(m)
+    n = int(rng.integers(1, 60))
+    ptm = rng.integers(0, 99, (n, m)).astype(np.int32)
+    pf, dp = inputs.pool_d1(n, 777, 100 + m)
+    compare(torch, fsp, orc, ptm, pf, dp)
+
+
+def test_parity_degenerate_instances(torch, fsp, orc):
+    rng = np.random.default_rng(9)
+    cases = [np.zeros((17, 6), np.int32),                           # all zero
+             np.tile(rng.integers(1, 99, 8), (40, 1)).astype(np.int32),   # identical jobs
+             rng.integers(0, 3, (33, 5)).astype(np.int32),           # heavy ties
+             rng.integers(0, 32767, (12, 4)).astype(np.int32),       # large times
+             np.array([[5, 7]], np.int32)]                           # n = 1
+    for ptm in cases:
+        n = ptm.shape[0]
+        pf, dp = inputs.pool_d1(n, 200, 3)
+        pf2, dp2 = inputs.pool_fixed_depth(n, 50, n, 4)
+        compare(torch, fsp, orc, ptm, np.concatenate([pf, pf2]), np.concatenate([dp, dp2]))
+
+
+def test_parity_strides_and_ragged(torch, fsp, orc):
+    n, m, seed = inputs.TAILLARD_SEEDS["ta021"]
+    ptm = inputs.taillard(n, m, seed)
+    for stride in (n, n + 3, 64):
+        for N in (1, 31, 33, 257, 1000):
+            pf, dp = inputs.pool_d1(n, N, N + stride, stride=stride)
+            compare(torch, fsp, orc, ptm, pf, dp)
+
+
+def test_duplicates_and_empty(torch, fsp, orc):
+    n, m, seed = inputs.TAILLARD_SEEDS["ta051"]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, 1, 77)
+    pf, dp = np.repeat(pf, 999, 0), np.repeat(dp, 999, 0)
+    compare(torch, fsp, orc, ptm, pf, dp)
+    inst = fsp.Instance(ptm)
+    import torch as T
+    out = inst.lb_eval(T.zeros((0, 56), dtype=T.int16, device="cuda"),
+                       T.zeros(0, dtype=T.int32, device="cuda"))
+    assert out.numel() == 0
+
+
+def test_malformed_nodes_flagged(torch, fsp, orc):
+    n, m, seed = inputs.TAILLARD_SEEDS["ta021"]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, 500, 8)
+    inst = fsp.Instance(ptm)
+    gpu_lb(torch, inst, pf, dp)
+    assert inst.check() == fsp.FSP_OK
+    want = orc.Tables(ptm).lb_eval(pf, dp)
+    for kind in ("job", "dup", "depth"):
+        bad_pf, bad_dp = pf.copy(), dp.copy()
+        i = 123
+        bad_dp[i] = max(bad_dp[i], 2)
+        bad_pf[i, :bad_dp[i]] = np.arange(bad_dp[i])
+        if kind == "job":
+            bad_pf[i, 0] = n + 5
+        elif kind == "dup":
+            bad_pf[i, 1] = bad_pf[i, 0]
+        else:
+            bad_dp[i] = n + 1
+        got = gpu_lb(torch, inst, bad_pf, bad_dp)
+        assert inst.check() == fsp.FSP_EBADNODE, kind
+        assert inst.check() == fsp.FSP_OK           # flag cleared
+        keep = np.arange(500) != i
+        assert (got[keep] == want[keep]).all(), kind
+
+
+def test_host_api_matches_device(torch, fsp, orc):
+    n, m, seed = inputs.TAILLARD_SEEDS["ta051"]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, 300_001, 31)
+    inst = fsp.Instance(ptm)
+    host = inst.lb_eval_host(pf, dp)
+    devv = gpu_lb(torch, inst, pf, dp)
+    assert (host == devv).all()
+    sample = np.random.default_rng(0).choice(len(dp), 2000, replace=False)
+    want = orc.Tables(ptm).lb_eval(pf[sample], dp[sample])
+    assert (host[sample] == want).all()
+
+
+def test_full_size_200x20_sampled(torch, fsp, orc):
+    """BASELINE configs[3] at bench size (1M nodes, bench launch config):
+    sampled nodes recomputed one by one by the oracle."""
+    n, m, seed = inputs.TAILLARD_SEEDS["ta091"]
+    ptm = inputs.taillard(n, m, seed)
+    N = 1 << 20
+    pf, dp = inputs.pool_d1(n, N, inputs.pool_seed("ta091"))
+    inst = fsp.Instance(ptm)
+    got = gpu_lb(torch, inst, pf, dp)
+    assert inst.check() == fsp.FSP_OK
+    rng = np.random.default_rng(1)
+    sample = np.concatenate([rng.choice(N, 3000, replace=False), np.arange(N - 40, N)])
+    want = orc.Tables(ptm).lb_eval(pf[sample], dp[sample])
+    assert (got[sample] == want).all()
+    # properties at any size: LB >= prefix-free machine bound, <= (n+m-1)*max p
+    assert got.min() >= int(ptm.sum(0).max()) and got.max() <= (n + m - 1) * int(ptm.max())
