@@ -9,17 +9,35 @@
 #include "fsp.h"
 
 // Per-(couple, position) record of the pair walk, staged in shared memory.
-//   c1   = p_{j,k} + lag_j(k,l)  = sum_{k<=i<l} p_{j,i}   (int32)
-//   meta = (c2 << 16) | (4*j),   c2 = p_{j,k} - p_{j,l}    (int16 in the top half)
+//   c1   = p_{j,k} + lag_j(k,l)  = sum_{k<=i<l} p_{j,i}        (int32)
+//   meta = (c2 << 16) | addr_j,  c2 = p_{j,k} - p_{j,l}         (int16, top half)
+//   addr_j = shared-window address of U[j][warp 0] (16 bits, see fsp_lb_layout)
 // j is the job at this position of the couple's Johnson-with-lags order.
 // DESIGN.md §6 derives the two-constant form of Fig. 3 lines 11-15.
+// Padding records after the last couple of a group (walk look-ahead).
+#define FSP_REC_SLACK 8
+
 struct __align__(8) fsp_rec {
     int32_t c1;
     int32_t meta;
 };
 
+// Dynamic shared-memory layout of the lb kernel (byte offsets).
+struct fsp_lb_layout {
+    size_t off_u, u_bytes;     // U[(n+1)][W] uint2 transposed unscheduled sets
+    size_t off_ptm, ptm_bytes; // PTM int32 [n][mp4]
+    size_t off_bar;            // mbarrier
+    size_t off_rt, rt_bytes;   // per warp: R[MAXM][64], T[MAXM][64] int32
+    size_t off_tab;            // one couple group: [kl header][records]
+    size_t kl_bytes, group_bytes;
+};
+
 struct fsp_lb_plan {
     int maxm;            // machine-count specialisation (template)
+    bool exact;          // maxm == m (5, 10, 20)
+    uint32_t smem_base;  // shared-window address of dynamic smem offset 0
+    int nrec;            // records per couple (n rounded up to even)
+    fsp_lb_layout L;
     int groups;          // couple groups (one resident in smem at a time)
     int pairs_per_group; // couples per group (last group may be shorter)
     int warps;           // warps per CTA
@@ -27,9 +45,6 @@ struct fsp_lb_plan {
     int num_sms;
     int grid;
     size_t smem_bytes;   // dynamic smem per CTA
-    size_t group_bytes;  // bytes of one group's blob (records + couple ids), 16-aligned
-    size_t ptm_bytes;    // u16 PTM staged in smem, 16-aligned
-    size_t warp_bytes;   // per-warp scratch
 };
 
 struct fsp_instance {
@@ -40,8 +55,8 @@ struct fsp_instance {
     int32_t *h_ptm;
     // device tables
     uint8_t *d_tables;   // groups * group_bytes: per group [pairs][n] fsp_rec then u32 couple ids
-    uint16_t *d_ptm16;   // [n][m] u16 (padded to ptm_bytes)
-    int32_t *d_ptm32;    // [n][m] int32 (B&B leaf makespans)
+    int32_t *d_ptm32s;   // [n][mp4] int32, padded rows (lb kernel smem image)
+    int32_t *d_ptm32;    // [n][m] int32 (B&B)
     int *d_err;          // malformed-node flag
     int64_t table_bytes;
     fsp_lb_plan plan;

@@ -19,8 +19,6 @@
 
 #include "fsp_internal.h"
 
-static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-
 extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_instance **out)
 {
     if (!ptm || !out) return fsp_fail(FSP_EINVAL, "null pointer");
@@ -61,18 +59,29 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
         return rc;
     }
     const fsp_lb_plan &pl = inst->plan;
-    const int P = inst->P;
 
-    // ---- couple tables, grouped: [u32 (k | l<<16) x ppg][fsp_rec x np x n] ----
+    // ---- couple tables, grouped: [u32 (k | l<<16) x ppg][fsp_rec x np x nrec] ----
     std::vector<int32_t> S((size_t)n * (m + 1));
     for (int j = 0; j < n; ++j) {
         S[(size_t)j * (m + 1)] = 0;
         for (int i = 0; i < m; ++i)
             S[(size_t)j * (m + 1) + i + 1] = S[(size_t)j * (m + 1) + i] + ptm[(size_t)j * m + i];
     }
-    const size_t gbytes = pl.group_bytes;
-    const size_t kl_bytes = align16((size_t)pl.pairs_per_group * 4);
+    const size_t gbytes = pl.L.group_bytes;
+    const size_t kl_bytes = pl.L.kl_bytes;
+    // shared address of U[j][warp 0]; row n is the always-empty padding row
+    auto uaddr = [&](int j) {
+        return (uint32_t)(pl.smem_base + pl.L.off_u + (size_t)j * 8 * pl.warps);
+    };
     std::vector<uint8_t> blob(gbytes * pl.groups, 0);
+    for (int g = 0; g < pl.groups; ++g) { // every record slot starts as padding
+        fsp_rec *rec = reinterpret_cast<fsp_rec *>(blob.data() + (size_t)g * gbytes + kl_bytes);
+        const size_t nslots = (gbytes - kl_bytes) / sizeof(fsp_rec);
+        for (size_t i = 0; i < nslots; ++i) {
+            rec[i].c1 = 0;
+            rec[i].meta = (int32_t)uaddr(n);
+        }
+    }
     std::vector<int> order(n), A(n), B(n);
     int p = 0;
     for (int k = 0; k < m; ++k) {
@@ -94,32 +103,31 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
                 if (fx ? A[x] != A[y] : B[x] != B[y]) return fx ? A[x] < A[y] : B[x] > B[y];
                 return x < y;
             });
-            fsp_rec *rec = reinterpret_cast<fsp_rec *>(gb + kl_bytes) + (size_t)pl_idx * n;
+            fsp_rec *rec = reinterpret_cast<fsp_rec *>(gb + kl_bytes) + (size_t)pl_idx * pl.nrec;
             for (int i = 0; i < n; ++i) {
                 const int j = order[i];
                 const int c2 = ptm[(size_t)j * m + k] - ptm[(size_t)j * m + l];
                 rec[i].c1 = A[j];
-                rec[i].meta = (int32_t)(((uint32_t)c2 << 16) | (uint32_t)(4 * j));
+                rec[i].meta = (int32_t)(((uint32_t)c2 << 16) | uaddr(j));
             }
         }
     }
-    (void)P;
 
-    // ---- PTM as u16 rows (stride mp, even) for shared memory; int32 copy ----
-    const int mp = (m + 1) & ~1;
-    std::vector<uint16_t> p16(pl.ptm_bytes / 2, 0);
+    // ---- PTM as int32 rows padded to mp4 (16-byte rows) for shared memory ----
+    const int mp4 = (m + 3) & ~3;
+    std::vector<int32_t> p32(pl.L.ptm_bytes / 4, 0);
     for (int j = 0; j < n; ++j)
-        for (int k = 0; k < m; ++k) p16[(size_t)j * mp + k] = (uint16_t)ptm[(size_t)j * m + k];
+        for (int k = 0; k < m; ++k) p32[(size_t)j * mp4 + k] = ptm[(size_t)j * m + k];
 
     inst->table_bytes = (int64_t)blob.size();
     e = cudaMalloc(&inst->d_tables, blob.size());
-    if (e == cudaSuccess) e = cudaMalloc(&inst->d_ptm16, pl.ptm_bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&inst->d_ptm32s, pl.L.ptm_bytes);
     if (e == cudaSuccess) e = cudaMalloc(&inst->d_ptm32, sizeof(int32_t) * (size_t)n * m);
     if (e == cudaSuccess) e = cudaMalloc(&inst->d_err, sizeof(int));
     if (e == cudaSuccess)
         e = cudaMemcpy(inst->d_tables, blob.data(), blob.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
-        e = cudaMemcpy(inst->d_ptm16, p16.data(), pl.ptm_bytes, cudaMemcpyHostToDevice);
+        e = cudaMemcpy(inst->d_ptm32s, p32.data(), pl.L.ptm_bytes, cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
         e = cudaMemcpy(inst->d_ptm32, ptm, sizeof(int32_t) * (size_t)n * m, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(inst->d_err, 0, sizeof(int));
@@ -138,7 +146,7 @@ extern "C" void fsp_instance_free(fsp_instance *inst)
     if (!inst) return;
     if (inst->host_ctx) fsp_host_ctx_free(inst->host_ctx);
     if (inst->d_tables) cudaFree(inst->d_tables);
-    if (inst->d_ptm16) cudaFree(inst->d_ptm16);
+    if (inst->d_ptm32s) cudaFree(inst->d_ptm32s);
     if (inst->d_ptm32) cudaFree(inst->d_ptm32);
     if (inst->d_err) cudaFree(inst->d_err);
     delete[] inst->h_ptm;

@@ -2,22 +2,25 @@
 //
 // Computes, for every node of a pool, the LB of Fig. 3 with the
 // readings R1-R6 of DESIGN.md §3.  Design:
-//   * one thread per sub-problem, as the paper maps it, 32 nodes per
-//     warp; every table read in the pair walk is then warp-uniform (broadcast);
+//   * one thread per sub-problem, as the paper maps it — here two
+//     sub-problems per thread, 64 per warp, so every table read of the couple
+//     walk is warp-uniform (a shared-memory broadcast) and feeds 64 nodes;
 //   * the per-couple tables (Johnson-with-lags order with each job's constants
 //     folded into an 8-byte record) are staged into shared memory by TMA bulk
 //     copies (cp.async.bulk + mbarrier), one couple group at a time when the
-//     whole set exceeds shared memory (200x20: 2 groups);
-//   * per warp, the unscheduled sets of its 32 nodes live in a transposed
-//     bitset U[job] (bit L = job unscheduled in lane L's node), built from
-//     coalesced reads of the prefix records;
+//     whole set exceeds shared memory (200x20: 3 groups);
+//   * the unscheduled sets of a warp's 64 nodes are a transposed bitset
+//     U[job][warp] = {bits of nodes 0-31, bits of nodes 32-63}, built from
+//     coalesced reads of the prefix records; each record carries the absolute
+//     shared address of U[job][0], so one LOP3 (| 8*warp) addresses it;
 //   * the walk of Fig. 3 lines 08-17 is carried in the (u, w) form
 //         u <- max(u, w + c1_j);  w <- w + c2_j      (if j unscheduled)
-//     two integer ops per update (VIADDMNMX + IADD), exact in int32.
+//     two predicated integer ops per update (VIADDMNMX + LEA.HI), exact int32.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <climits>
+#include <cstdlib>
 
 #include "fsp_internal.h"
 
@@ -81,54 +84,82 @@ __device__ __forceinline__ void bulk_copy(void *dst, const void *src, uint32_t b
     }
 }
 
+__device__ __forceinline__ uint2 lds_u2(uint32_t addr)
+{
+    uint2 v;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+
 struct LbArgs {
     const uint8_t *tables; // groups x group_bytes
-    const uint16_t *ptm16; // [n][mp] u16, ptm_bytes
+    const int32_t *ptm;    // [n][mp4] int32, ptm_bytes
     const uint16_t *prefix;
     const int32_t *depth;
     int32_t *lb_out;
     int *err;
     long long pool;
-    unsigned long long group_bytes;
-    int ptm_bytes;
-    int warp_bytes;
+    uint32_t smem_base;    // shared-window address the host baked into the records
+    fsp_lb_layout L;
     int groups, ppg;       // couple groups, couples per group
-    int n, m, P, mp;       // mp = PTM row stride in u16 (even)
+    int n, m, P, mp4, nrec;
     int stride;
-    int kl_bytes;          // couple-id header bytes of a group blob
 };
 
-template <int MAXM>
+// One (u, w) update of Fig. 3 lines 10-15 for the two nodes of this lane,
+// given the U masks MASK of the record's job: line 10 is the predicate.
+#define FSP_UPD(MASK, C1, META)                                                 \
+    {                                                                           \
+        if ((MASK).x & lanebit) {                                               \
+            asm volatile(""); /* keep a branch: ptxas predicates it */          \
+            u0 = max(u0, w0 + (int)(C1));                                       \
+            w0 += ((int)(META) >> 16);                                          \
+        }                                                                       \
+        if ((MASK).y & lanebit) {                                               \
+            asm volatile("");                                                   \
+            u1 = max(u1, w1 + (int)(C1));                                       \
+            w1 += ((int)(META) >> 16);                                          \
+        }                                                                       \
+    }
+#define FSP_MASK(META) lds_u2(((uint32_t)(META) & 0xffffu) | w8)
+
+template <int MAXM, bool EXACT>
 __global__ void __launch_bounds__(256) lb_kernel(const LbArgs a)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    const int n = a.n, m = a.m;
-    uint8_t *s_tab = smem;
-    const uint16_t *s_ptm = reinterpret_cast<const uint16_t *>(smem + a.group_bytes);
-    uint64_t *s_bar = reinterpret_cast<uint64_t *>(smem + a.group_bytes + a.ptm_bytes);
+    const int n = a.n;
+    const int m = EXACT ? MAXM : a.m;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int W = blockDim.x >> 5;
-    uint8_t *s_warp = smem + a.group_bytes + a.ptm_bytes + 16 + (size_t)warp * a.warp_bytes;
-    uint32_t *U = reinterpret_cast<uint32_t *>(s_warp);
-    const int ubytes = ((n * 4) + 15) & ~15;
-    int *Rs = reinterpret_cast<int *>(s_warp + ubytes); // [MAXM][32] heads
-    int *Ts = Rs + MAXM * 32;                            // [MAXM][32] tail + load
+    uint32_t *Uw = reinterpret_cast<uint32_t *>(smem + a.L.off_u);      // [(n+1)][W][2]
+    const int32_t *s_ptm = reinterpret_cast<const int32_t *>(smem + a.L.off_ptm);
+    uint64_t *s_bar = reinterpret_cast<uint64_t *>(smem + a.L.off_bar);
+    int *Rs = reinterpret_cast<int *>(smem + a.L.off_rt + (size_t)warp * a.L.rt_bytes);
+    int *Ts = Rs + MAXM * 64;                                            // [MAXM][64]
+    uint8_t *s_tab = smem + a.L.off_tab;
+
+    if (smem_u32(smem) != a.smem_base) { // records carry absolute shared addresses
+        if (threadIdx.x == 0) atomicOr(a.err, 2);
+        return;
+    }
 
     auto group_size = [&](int g) {
         int np = a.P - g * a.ppg;
         return np < a.ppg ? np : a.ppg;
     };
     auto group_blob = [&](int g) {
-        return (uint32_t)((a.kl_bytes + (size_t)group_size(g) * n * sizeof(fsp_rec) + 15) & ~size_t(15));
+        return (uint32_t)((a.L.kl_bytes +
+                           ((size_t)group_size(g) * a.nrec + FSP_REC_SLACK) * sizeof(fsp_rec) + 15) &
+                          ~size_t(15));
     };
 
     // ---- stage PTM + the first couple group (TMA bulk, one mbarrier) ----
     if (threadIdx.x == 0) {
         mbar_init(s_bar, 1);
         uint32_t gb = group_blob(0);
-        mbar_expect_tx(s_bar, gb + (uint32_t)a.ptm_bytes);
+        mbar_expect_tx(s_bar, gb + (uint32_t)a.L.ptm_bytes);
         bulk_copy(s_tab, a.tables, gb, s_bar);
-        bulk_copy(const_cast<uint16_t *>(s_ptm), a.ptm16, (uint32_t)a.ptm_bytes, s_bar);
+        bulk_copy(smem + a.L.off_ptm, a.ptm, (uint32_t)a.L.ptm_bytes, s_bar);
     }
     __syncthreads();
     uint32_t phase = 0;
@@ -136,135 +167,142 @@ __global__ void __launch_bounds__(256) lb_kernel(const LbArgs a)
     phase ^= 1;
     int resident = 0;
 
-    const long long ntiles = (a.pool + 31) >> 5;
+    const long long ntiles = (a.pool + 63) >> 6;
     const long long nchunks = (ntiles + W - 1) / W;
     const uint32_t lanebit = 1u << lane;
+    const uint32_t w8 = 8u * warp;
 
     for (long long chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
         const long long tile = chunk * W + warp;
-        const long long node = tile * 32 + lane;
-        const bool has = node < a.pool;
+        const long long node0 = tile * 64 + lane, node1 = node0 + 32;
+        const bool has0 = node0 < a.pool, has1 = node1 < a.pool;
         bool bad = false;
 
         // ---------------- a1: node ingest (depth, scheduled set) ----------------
-        int d = 0;
-        if (has) {
-            d = a.depth[node];
-            if (d < 0 || d > n || d > a.stride) {
-                bad = true;
-                d = 0;
-            }
+        int d0 = 0, d1 = 0;
+        if (has0) d0 = a.depth[node0];
+        if (has1) d1 = a.depth[node1];
+        if (d0 < 0 || d0 > n || d0 > a.stride) { bad = true; d0 = 0; }
+        if (d1 < 0 || d1 > n || d1 > a.stride) { bad = true; d1 = 0; }
+        const uint32_t valid0 = __ballot_sync(0xffffffffu, has0);
+        const uint32_t valid1 = __ballot_sync(0xffffffffu, has1);
+        for (int j = lane; j <= n; j += 32) {
+            Uw[(j * W + warp) * 2 + 0] = j < n ? valid0 : 0u; // row n: the padding record's
+            Uw[(j * W + warp) * 2 + 1] = j < n ? valid1 : 0u; // always-empty mask
         }
-        const uint32_t valid = __ballot_sync(0xffffffffu, has);
-        for (int j = lane; j < n; j += 32) U[j] = valid;
         __syncwarp();
-        // coalesced pass over the 32 prefix records: clear the scheduled bits
-        for (int L = 0; L < 32; ++L) {
-            const int dL = __shfl_sync(0xffffffffu, d, L);
+        // coalesced pass over the 64 prefix records: clear the scheduled bits
+        for (int L = 0; L < 64; ++L) {
+            const int dL = __shfl_sync(0xffffffffu, L < 32 ? d0 : d1, L & 31);
             if (dL == 0) continue;
-            const uint16_t *row = a.prefix + (size_t)(tile * 32 + L) * a.stride;
+            const uint16_t *row = a.prefix + (size_t)(tile * 64 + L) * a.stride;
+            const uint32_t clr = ~(1u << (L & 31));
             for (int i = lane; i < dL; i += 32) {
                 const uint32_t job = row[i];
-                if (job < (uint32_t)n) U[job] &= ~(1u << L);
+                if (job < (uint32_t)n) Uw[(job * W + warp) * 2 + (L >> 5)] &= clr;
             }
             __syncwarp();
         }
 
-        // prefix completion times C_k, one node per lane
-        int C[MAXM];
+        // ---------------- per node of this lane: C, heads, tails ----------------
+#pragma unroll 1
+        for (int q = 0; q < 2; ++q) {
+            const long long node = q ? node1 : node0;
+            const int d = q ? d1 : d0;
+            // prefix completion times C_k
+            int C[MAXM];
 #pragma unroll
-        for (int k = 0; k < MAXM; ++k) C[k] = 0;
-        {
-            const uint16_t *row = a.prefix + (size_t)(has ? node : 0) * a.stride;
+            for (int k = 0; k < MAXM; ++k) C[k] = 0;
+            const uint16_t *row = a.prefix + (size_t)(d ? node : 0) * a.stride;
             for (int i = 0; i < d; ++i) {
                 uint32_t job = row[i];
-                if (job >= (uint32_t)n) {
-                    bad = true;
-                    job = 0;
-                }
-                const uint32_t *pr = reinterpret_cast<const uint32_t *>(s_ptm + job * a.mp);
+                if (job >= (uint32_t)n) { bad = true; job = 0; }
+                const int4 *pr = reinterpret_cast<const int4 *>(s_ptm + job * a.mp4);
                 int prev = 0;
 #pragma unroll
-                for (int k2 = 0; k2 < (MAXM + 1) / 2; ++k2) {
-                    const uint32_t w2 = 2 * k2 < m ? pr[k2] : 0u;
-                    if (2 * k2 < m) {
-                        C[2 * k2] = max(C[2 * k2], prev) + (int)(w2 & 0xffffu);
-                        prev = C[2 * k2];
+                for (int k4 = 0; k4 < (MAXM + 3) / 4; ++k4) {
+                    if (4 * k4 < m) {
+                        const int4 v = pr[k4];
+                        const int pv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const int k = 4 * k4 + t;
+                            if (k < MAXM && k < m) {
+                                C[k] = max(C[k], prev) + pv[t];
+                                prev = C[k];
+                            }
+                        }
                     }
-                    if (2 * k2 + 1 < MAXM && 2 * k2 + 1 < m) {
-                        C[2 * k2 + 1] = max(C[2 * k2 + 1], prev) + (int)(w2 >> 16);
-                        prev = C[2 * k2 + 1];
-                    }
                 }
             }
-        }
-
-        // ---------------- a2/a3: heads R_k, tails Q_l, loads L_l ----------------
-        // r_j0 = C_0, r_jk = max(C_k, r_j,k-1 + p_j,k-1) (R3); R_k = min over
-        // unscheduled j (R5); q_jl = sum_{i>l} p_ji, Q_l = min (R4); and the
-        // remaining load L_l = sum_j p_jl that closes the (u, w) walk.
-        int R[MAXM], Q[MAXM], Ld[MAXM];
-#pragma unroll
-        for (int k = 0; k < MAXM; ++k) {
-            R[k] = INT_MAX;
-            Q[k] = INT_MAX;
-            Ld[k] = 0;
-        }
-        int cnt = 0;
-        for (int j = 0; j < n; ++j) {
-            const uint32_t uj = U[j];
-            if (uj == 0) continue; // scheduled in every node of this warp
-            const int act = (uj >> lane) & 1;
-            const int nm = act ? 0 : INT_MAX;
-            cnt += act;
-            const uint32_t *pr = reinterpret_cast<const uint32_t *>(s_ptm + j * a.mp);
-            int p[MAXM];
-#pragma unroll
-            for (int k2 = 0; k2 < (MAXM + 1) / 2; ++k2) {
-                const uint32_t w2 = 2 * k2 < m ? pr[k2] : 0u;
-                p[2 * k2] = (int)(w2 & 0xffffu);
-                if (2 * k2 + 1 < MAXM) p[2 * k2 + 1] = (int)(w2 >> 16);
-            }
-            int r = C[0];
-            R[0] = min(R[0], r | nm);
-#pragma unroll
-            for (int k = 1; k < MAXM; ++k) {
-                if (k < m) {
-                    r = max(C[k], r + p[k - 1]);
-                    R[k] = min(R[k], r | nm);
-                }
-            }
-            int q = 0;
-#pragma unroll
-            for (int l = MAXM - 1; l >= 0; --l) {
-                if (l < m) {
-                    Q[l] = min(Q[l], q | nm);
-                    q += p[l];
-                    Ld[l] += act * p[l];
-                }
-            }
-        }
-        if (has && cnt != n - d) bad = true; // repeated or out-of-range job
-        if (cnt == 0) {                       // R6: complete schedule
+            // a2/a3: r_j0 = C_0, r_jk = max(C_k, r_j,k-1 + p_j,k-1) (R3); R_k =
+            // min over unscheduled j (R5); Q_l = min_j q_jl, q_jl = sum_{i>l}
+            // p_ji (R4); L_l = sum_j p_jl closes the (u, w) walk.
+            int R[MAXM], Q[MAXM], Ld[MAXM];
 #pragma unroll
             for (int k = 0; k < MAXM; ++k) {
-                R[k] = C[k];
-                Q[k] = 0;
+                R[k] = INT_MAX;
+                Q[k] = INT_MAX;
                 Ld[k] = 0;
             }
-        }
+            int cnt = 0;
+            for (int j = 0; j < n; ++j) {
+                const uint32_t uj = Uw[(j * W + warp) * 2 + q];
+                if (uj == 0) continue; // scheduled in every node of this half-warp
+                if (uj & lanebit) {
+                    ++cnt;
+                    const int4 *pr = reinterpret_cast<const int4 *>(s_ptm + j * a.mp4);
+                    int p[MAXM];
 #pragma unroll
-        for (int k = 0; k < MAXM; ++k) {
-            if (k < m) {
-                Rs[k * 32 + lane] = R[k];
-                Ts[k * 32 + lane] = Q[k] + Ld[k];
+                    for (int k4 = 0; k4 < (MAXM + 3) / 4; ++k4) {
+                        const int4 v = 4 * k4 < m ? pr[k4] : make_int4(0, 0, 0, 0);
+                        if (4 * k4 + 0 < MAXM) p[4 * k4 + 0] = v.x;
+                        if (4 * k4 + 1 < MAXM) p[4 * k4 + 1] = v.y;
+                        if (4 * k4 + 2 < MAXM) p[4 * k4 + 2] = v.z;
+                        if (4 * k4 + 3 < MAXM) p[4 * k4 + 3] = v.w;
+                    }
+                    int r = C[0];
+                    R[0] = min(R[0], r);
+#pragma unroll
+                    for (int k = 1; k < MAXM; ++k) {
+                        if (k < m) {
+                            r = max(C[k], r + p[k - 1]);
+                            R[k] = min(R[k], r);
+                        }
+                    }
+                    int qq = 0;
+#pragma unroll
+                    for (int l = MAXM - 1; l >= 0; --l) {
+                        if (l < m) {
+                            Q[l] = min(Q[l], qq);
+                            qq += p[l];
+                            Ld[l] += p[l];
+                        }
+                    }
+                }
+            }
+            if ((q ? has1 : has0) && cnt != n - d) bad = true; // repeated / bad job
+            if (cnt == 0) { // R6: complete schedule
+#pragma unroll
+                for (int k = 0; k < MAXM; ++k) {
+                    R[k] = C[k];
+                    Q[k] = 0;
+                    Ld[k] = 0;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < MAXM; ++k) {
+                if (k < m) {
+                    Rs[k * 64 + q * 32 + lane] = R[k];
+                    Ts[k * 64 + q * 32 + lane] = Q[k] + Ld[k];
+                }
             }
         }
         if (bad) atomicOr(a.err, 1);
         __syncwarp();
 
         // ---------------- a4/a5: couple walks (Fig. 3 lines 03-19) ----------------
-        int lb = 0; // R1
+        int lb0 = 0, lb1 = 0; // R1
         const bool ascending = resident == 0;
         for (int gi = 0; gi < a.groups; ++gi) {
             const int g = ascending ? gi : a.groups - 1 - gi;
@@ -274,60 +312,77 @@ __global__ void __launch_bounds__(256) lb_kernel(const LbArgs a)
                     fence_proxy_async();
                     const uint32_t gb = group_blob(g);
                     mbar_expect_tx(s_bar, gb);
-                    bulk_copy(s_tab, a.tables + (size_t)g * a.group_bytes, gb, s_bar);
+                    bulk_copy(s_tab, a.tables + (size_t)g * a.L.group_bytes, gb, s_bar);
                 }
                 mbar_wait(s_bar, phase);
                 phase ^= 1;
                 resident = g;
             }
-            if (valid == 0) continue;
+            if ((valid0 | valid1) == 0) continue;
             const uint32_t *kl = reinterpret_cast<const uint32_t *>(s_tab);
-            const fsp_rec *recs = reinterpret_cast<const fsp_rec *>(s_tab + a.kl_bytes);
+            const uint4 *recs = reinterpret_cast<const uint4 *>(s_tab + a.L.kl_bytes);
             const int np = group_size(g);
-            const char *ub = reinterpret_cast<const char *>(U);
+            const int n2 = a.nrec >> 1, n4 = a.nrec >> 2;
             for (int pl = 0; pl < np; ++pl) {
                 const uint32_t kv = kl[pl];
                 const int k = kv & 0xffff, l = kv >> 16;
-                int u = Rs[l * 32 + lane]; // timeOnM2 starts at RM min of M2 (line 07)
-                int w = Rs[k * 32 + lane]; // timeOnM1 starts at RM min of M1 (line 06)
-                const fsp_rec *rp = recs + (size_t)pl * n;
-#pragma unroll 8
-                for (int i = 0; i < n; ++i) {
-                    const fsp_rec r = rp[i];
-                    const uint32_t msk =
-                        *reinterpret_cast<const uint32_t *>(ub + (r.meta & 0xffff));
-                    if (msk & lanebit) { // line 10: job not yet scheduled
-                        u = max(u, w + r.c1);   // lines 11-15, (u, w) form
-                        w += (r.meta >> 16);
-                    }
+                // lines 06-07: timeOnM1 / timeOnM2 start at the RM minima
+                int u0 = Rs[l * 64 + lane], u1 = Rs[l * 64 + 32 + lane];
+                int w0 = Rs[k * 64 + lane], w1 = Rs[k * 64 + 32 + lane];
+                const uint4 *rp = recs + (size_t)pl * n2;
+                // lines 08-17, software-pipelined 4 positions per step: records
+                // two steps ahead, U masks one step ahead (the group blob ends
+                // with padding records so the look-ahead stays in bounds).
+                uint4 ra = rp[0], rb = rp[1], na = rp[2], nb = rp[3];
+                uint2 ma = FSP_MASK(ra.y), mb = FSP_MASK(ra.w);
+                uint2 mc = FSP_MASK(rb.y), md = FSP_MASK(rb.w);
+                for (int it = 0; it < n4; ++it) {
+                    const uint4 fa = rp[2 * it + 4], fb = rp[2 * it + 5];
+                    const uint2 xa = FSP_MASK(na.y), xb = FSP_MASK(na.w);
+                    const uint2 xc = FSP_MASK(nb.y), xd = FSP_MASK(nb.w);
+                    FSP_UPD(ma, ra.x, ra.y);
+                    FSP_UPD(mb, ra.z, ra.w);
+                    FSP_UPD(mc, rb.x, rb.y);
+                    FSP_UPD(md, rb.z, rb.w);
+                    ra = na; rb = nb; na = fa; nb = fb;
+                    ma = xa; mb = xb; mc = xc; md = xd;
                 }
-                lb = max(lb, u + Ts[l * 32 + lane]); // lines 18-19
+                lb0 = max(lb0, u0 + Ts[l * 64 + lane]); // lines 18-19
+                lb1 = max(lb1, u1 + Ts[l * 64 + 32 + lane]);
             }
         }
-        if (has) a.lb_out[node] = lb;
+        if (has0) a.lb_out[node0] = lb0;
+        if (has1) a.lb_out[node1] = lb1;
         __syncwarp();
     }
 }
 
-template <int MAXM>
+__global__ void smem_base_probe(uint32_t *out)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    *out = smem_u32(smem);
+}
+
+template <int MAXM, bool EXACT>
 int launch(const fsp_instance *inst, const LbArgs &a, cudaStream_t s)
 {
     const fsp_lb_plan &pl = inst->plan;
-    lb_kernel<MAXM><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
+    lb_kernel<MAXM, EXACT><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, "lb_kernel launch");
 }
 
-template <int MAXM>
+template <int MAXM, bool EXACT>
 int configure(fsp_instance *inst)
 {
     fsp_lb_plan &pl = inst->plan;
-    cudaError_t e = cudaFuncSetAttribute(lb_kernel<MAXM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(lb_kernel<MAXM, EXACT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)pl.smem_bytes);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "cudaFuncSetAttribute");
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM>, pl.warps * 32,
-                                                      pl.smem_bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM, EXACT>,
+                                                      pl.warps * 32, pl.smem_bytes);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "occupancy");
     if (per_sm < 1) return fsp_fail(FSP_ERANGE, "lb kernel does not fit on an SM");
     pl.ctas_per_sm = per_sm;
@@ -335,57 +390,91 @@ int configure(fsp_instance *inst)
     return FSP_OK;
 }
 
+// (MAXM, EXACT) specialisations: exact for Taillard's 5/10/20 machines.
+#define FSP_DISPATCH(FN, ...)                                                   \
+    switch (pl.maxm * 2 + (pl.exact ? 1 : 0)) {                                 \
+    case 5 * 2 + 1: return FN<5, true>(__VA_ARGS__);                            \
+    case 10 * 2 + 1: return FN<10, true>(__VA_ARGS__);                          \
+    case 20 * 2 + 1: return FN<20, true>(__VA_ARGS__);                          \
+    case 8 * 2: return FN<8, false>(__VA_ARGS__);                               \
+    case 16 * 2: return FN<16, false>(__VA_ARGS__);                             \
+    case 24 * 2: return FN<24, false>(__VA_ARGS__);                             \
+    default: return FN<32, false>(__VA_ARGS__);                                 \
+    }
+
 } // namespace
 
 static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Choose the machine specialisation, couple groups and CTA shape so that one
-// couple group + PTM + per-warp scratch fit the opt-in shared memory.
+static int probe_smem_base(uint32_t *base)
+{
+    uint32_t *d = nullptr, h = 0;
+    cudaError_t e = cudaMalloc(&d, sizeof(uint32_t));
+    if (e == cudaSuccess) {
+        smem_base_probe<<<1, 1, 16>>>(d);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(&h, d, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return fsp_cuda_fail(e, "smem base probe");
+    *base = h;
+    return FSP_OK;
+}
+
+// Choose the machine specialisation, warps per CTA and couple groups so that
+// one couple group + PTM + U + per-warp scratch fit the opt-in shared memory
+// and every U address fits the 16-bit record field.
 int fsp_plan_lb(fsp_instance *inst)
 {
     fsp_lb_plan &pl = inst->plan;
     const int n = inst->n, m = inst->m, P = inst->P;
-    static const int maxms[] = {5, 8, 10, 16, 20, 32};
-    pl.maxm = 0;
-    for (int mm : maxms)
-        if (m <= mm) {
-            pl.maxm = mm;
-            break;
-        }
-    if (!pl.maxm) return fsp_fail(FSP_ERANGE, "m too large");
+    pl.exact = (m == 5 || m == 10 || m == 20);
+    if (pl.exact) pl.maxm = m;
+    else if (m <= 8) pl.maxm = 8;
+    else if (m <= 16) pl.maxm = 16;
+    else if (m <= 24) pl.maxm = 24;
+    else if (m <= 32) pl.maxm = 32;
+    else return fsp_fail(FSP_ERANGE, "m too large");
     int dev = inst->device, optin = 0, sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "device attribute");
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "device attribute");
+    int rc = probe_smem_base(&pl.smem_base);
+    if (rc != FSP_OK) return rc;
     pl.num_sms = sms;
-    const int mp = (m + 1) & ~1;
-    pl.ptm_bytes = align16((size_t)n * mp * 2);
-    pl.warp_bytes = align16((size_t)n * 4) + 2 * (size_t)pl.maxm * 32 * 4;
+    const int mp4 = (m + 3) & ~3;
+    pl.nrec = (n + 3) & ~3; // walk steps of 4 positions
     int want_warps = 8;
     if (const char *s = getenv("FSP_LB_WARPS")) want_warps = atoi(s);
     if (want_warps < 1) want_warps = 1;
     if (want_warps > 8) want_warps = 8;
-    for (int W = want_warps; W >= 1; W /= 2) {
+    for (int W = want_warps; W >= 1; --W) {
+        fsp_lb_layout L{};
+        L.u_bytes = align16((size_t)(n + 1) * 8 * W);
+        if (pl.smem_base + (size_t)(n + 1) * 8 * W > 65536) continue; // 16-bit U addresses
+        L.off_u = 0;
+        L.ptm_bytes = align16((size_t)n * mp4 * 4);
+        L.off_ptm = L.u_bytes;
+        L.off_bar = L.off_ptm + L.ptm_bytes;
+        L.rt_bytes = 2 * (size_t)pl.maxm * 64 * 4;
+        L.off_rt = L.off_bar + 16;
+        L.off_tab = align16(L.off_rt + (size_t)W * L.rt_bytes);
         for (int G = 1; G <= P; ++G) {
             const int ppg = (P + G - 1) / G;
             const int Greal = (P + ppg - 1) / ppg;
-            const size_t gb = align16((size_t)ppg * 4) + (size_t)ppg * n * sizeof(fsp_rec);
-            const size_t total = gb + pl.ptm_bytes + 16 + (size_t)W * pl.warp_bytes;
-            if (total <= (size_t)optin) {
+            L.kl_bytes = align16((size_t)ppg * 4);
+            // + FSP_REC_SLACK padding records for the walk's look-ahead
+            const size_t gb =
+                align16(L.kl_bytes + ((size_t)ppg * pl.nrec + FSP_REC_SLACK) * sizeof(fsp_rec));
+            if (L.off_tab + gb <= (size_t)optin) {
+                L.group_bytes = gb;
+                pl.L = L;
                 pl.groups = Greal;
                 pl.pairs_per_group = ppg;
                 pl.warps = W;
-                pl.group_bytes = align16(gb);
-                pl.smem_bytes = pl.group_bytes + pl.ptm_bytes + 16 + (size_t)W * pl.warp_bytes;
-                switch (pl.maxm) {
-                case 5: return configure<5>(inst);
-                case 8: return configure<8>(inst);
-                case 10: return configure<10>(inst);
-                case 16: return configure<16>(inst);
-                case 20: return configure<20>(inst);
-                default: return configure<32>(inst);
-                }
+                pl.smem_bytes = L.off_tab + gb;
+                FSP_DISPATCH(configure, inst);
             }
             if (ppg == 1) break;
         }
@@ -399,29 +488,21 @@ int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stri
     const fsp_lb_plan &pl = inst->plan;
     LbArgs a;
     a.tables = inst->d_tables;
-    a.ptm16 = inst->d_ptm16;
+    a.ptm = inst->d_ptm32s;
     a.prefix = prefix;
     a.depth = depth;
     a.lb_out = lb_out;
     a.err = inst->d_err;
     a.pool = pool;
-    a.group_bytes = pl.group_bytes;
-    a.ptm_bytes = (int)pl.ptm_bytes;
-    a.warp_bytes = (int)pl.warp_bytes;
+    a.smem_base = pl.smem_base;
+    a.L = pl.L;
     a.groups = pl.groups;
     a.ppg = pl.pairs_per_group;
     a.n = inst->n;
     a.m = inst->m;
     a.P = inst->P;
-    a.mp = (inst->m + 1) & ~1;
+    a.mp4 = (inst->m + 3) & ~3;
+    a.nrec = pl.nrec;
     a.stride = stride;
-    a.kl_bytes = (int)align16((size_t)pl.pairs_per_group * 4);
-    switch (pl.maxm) {
-    case 5: return launch<5>(inst, a, s);
-    case 8: return launch<8>(inst, a, s);
-    case 10: return launch<10>(inst, a, s);
-    case 16: return launch<16>(inst, a, s);
-    case 20: return launch<20>(inst, a, s);
-    default: return launch<32>(inst, a, s);
-    }
+    FSP_DISPATCH(launch, inst, a, s);
 }
