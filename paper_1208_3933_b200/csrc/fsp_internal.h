@@ -10,8 +10,8 @@
 
 // Per-(couple, position) record of the pair walk, staged in shared memory.
 //   c1   = p_{j,k} + lag_j(k,l)  = sum_{k<=i<l} p_{j,i}        (int32)
-//   meta = (c2 << 16) | addr_j,  c2 = p_{j,k} - p_{j,l}         (int16, top half)
-//   addr_j = shared-window address of U[j][warp 0] (16 bits, see fsp_lb_layout)
+//   meta = (c2 << 16) | addr_j   (int32 walk)  or  (addr_j << 16) | (c2 & 0xffff) (s16 walk)
+//   c2 = p_{j,k} - p_{j,l} (int16); addr_j = shared-window address of U[j][warp 0]
 // j is the job at this position of the couple's Johnson-with-lags order.
 // DESIGN.md §6 derives the two-constant form of Fig. 3 lines 11-15.
 // Padding records after the last couple of a group (walk look-ahead).
@@ -35,6 +35,7 @@ struct fsp_lb_layout {
 struct fsp_lb_plan {
     int maxm;            // machine-count specialisation (template)
     bool exact;          // maxm == m (5, 10, 20)
+    bool s16;            // 16-bit walk (records in the s16 meta form)
     uint32_t smem_base;  // shared-window address of dynamic smem offset 0
     int nrec;            // records per couple (n rounded up to even)
     fsp_lb_layout L;

@@ -79,7 +79,7 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
         const size_t nslots = (gbytes - kl_bytes) / sizeof(fsp_rec);
         for (size_t i = 0; i < nslots; ++i) {
             rec[i].c1 = 0;
-            rec[i].meta = (int32_t)uaddr(n);
+            rec[i].meta = pl.s16 ? (int32_t)(uaddr(n) << 16) : (int32_t)uaddr(n);
         }
     }
     std::vector<int> order(n), A(n), B(n);
@@ -108,7 +108,8 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
                 const int j = order[i];
                 const int c2 = ptm[(size_t)j * m + k] - ptm[(size_t)j * m + l];
                 rec[i].c1 = A[j];
-                rec[i].meta = (int32_t)(((uint32_t)c2 << 16) | uaddr(j));
+                rec[i].meta = pl.s16 ? (int32_t)((uaddr(j) << 16) | ((uint32_t)c2 & 0xffffu))
+                                     : (int32_t)(((uint32_t)c2 << 16) | uaddr(j));
             }
         }
     }

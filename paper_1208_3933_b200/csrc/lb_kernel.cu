@@ -21,6 +21,7 @@
 
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 
 #include "fsp_internal.h"
 
@@ -104,27 +105,53 @@ struct LbArgs {
     int groups, ppg;       // couple groups, couples per group
     int n, m, P, mp4, nrec;
     int stride;
+    uint32_t hi_mul;       // 0x10000 (see mask_addr)
 };
 
-// One (u, w) update of Fig. 3 lines 10-15 for the two nodes of this lane,
-// given the U masks MASK of the record's job: line 10 is the predicate.
+// Shared address of U[job][warp] from a record's meta word.
+//   int32 form: meta = (c2 << 16) | addr    -> (meta & 0xffff) | 8*warp  (one LOP3)
+//   s16 form:   meta = (addr << 16) | c2    -> (meta >> 16) + 8*warp     (one IMAD.HI)
+// (hi_mul = 0x10000 arrives as a kernel argument so ptxas keeps an IMAD.HI on
+// the FMA pipe instead of strength-reducing it to an ALU LEA.HI: the ALU pipe
+// is the walk's bottleneck.)
+template <bool S16>
+__device__ __forceinline__ uint32_t mask_addr(uint32_t meta, uint32_t w8, uint32_t hi_mul)
+{
+    if constexpr (S16) return __umulhi(meta, hi_mul) + w8;
+    else return (meta & 0xffffu) | w8;
+}
+
+// One update of Fig. 3 lines 10-15 in the (u, w) form for one node; line 10
+// ("job not yet scheduled") is the predicate (a short branch ptxas predicates).
+//   int32: u = max(u, w + c1);  w += c2 (top half of meta, LEA.HI.SX32)
+//   s16:   the low halfwords carry u and w (all values fit int16, host-checked);
+//          u = max.s16(u, w + c1) (VIADDMNMX.S16x2), w += meta (low half += c2,
+//          the high halves only collect garbage that never reaches the low ones)
+template <bool S16>
+__device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1, uint32_t meta,
+                                    int &u, int &w)
+{
+    if (bits & lanebit) {
+        asm volatile(""); // keep the branch so ptxas predicates the two ops
+        if constexpr (S16) {
+            u = (int)__viaddmax_s16x2((unsigned)w, c1, (unsigned)u);
+            w += (int)meta;
+        } else {
+            u = max(u, w + (int)c1);
+            w += ((int)meta >> 16);
+        }
+    }
+}
+
+#define FSP_MASK(META) lds_u2(mask_addr<S16>((META), w8, hi_mul))
 #define FSP_UPD(MASK, C1, META)                                                 \
     {                                                                           \
-        if ((MASK).x & lanebit) {                                               \
-            asm volatile(""); /* keep a branch: ptxas predicates it */          \
-            u0 = max(u0, w0 + (int)(C1));                                       \
-            w0 += ((int)(META) >> 16);                                          \
-        }                                                                       \
-        if ((MASK).y & lanebit) {                                               \
-            asm volatile("");                                                   \
-            u1 = max(u1, w1 + (int)(C1));                                       \
-            w1 += ((int)(META) >> 16);                                          \
-        }                                                                       \
+        upd<S16>((MASK).x, lanebit, (C1), (META), u0, w0);                      \
+        upd<S16>((MASK).y, lanebit, (C1), (META), u1, w1);                      \
     }
-#define FSP_MASK(META) lds_u2(((uint32_t)(META) & 0xffffu) | w8)
 
-template <int MAXM, bool EXACT>
-__global__ void __launch_bounds__(256) lb_kernel(const LbArgs a)
+template <int MAXM, bool EXACT, bool S16>
+__global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs a)
 {
     extern __shared__ __align__(128) uint8_t smem[];
     const int n = a.n;
@@ -134,8 +161,11 @@ __global__ void __launch_bounds__(256) lb_kernel(const LbArgs a)
     uint32_t *Uw = reinterpret_cast<uint32_t *>(smem + a.L.off_u);      // [(n+1)][W][2]
     const int32_t *s_ptm = reinterpret_cast<const int32_t *>(smem + a.L.off_ptm);
     uint64_t *s_bar = reinterpret_cast<uint64_t *>(smem + a.L.off_bar);
-    int *Rs = reinterpret_cast<int *>(smem + a.L.off_rt + (size_t)warp * a.L.rt_bytes);
-    int *Ts = Rs + MAXM * 64;                                            // [MAXM][64]
+    // per-warp heads R[MAXM][64] and tail+load T[MAXM][64]; int16 in the s16
+    // walk (all values fit, host-checked), int32 otherwise
+    using rt_t = typename std::conditional<S16, int16_t, int32_t>::type;
+    rt_t *Rs = reinterpret_cast<rt_t *>(smem + a.L.off_rt + (size_t)warp * a.L.rt_bytes);
+    rt_t *Ts = Rs + MAXM * 64;
     uint8_t *s_tab = smem + a.L.off_tab;
 
     if (smem_u32(smem) != a.smem_base) { // records carry absolute shared addresses
@@ -171,6 +201,7 @@ __global__ void __launch_bounds__(256) lb_kernel(const LbArgs a)
     const long long nchunks = (ntiles + W - 1) / W;
     const uint32_t lanebit = 1u << lane;
     const uint32_t w8 = 8u * warp;
+    const uint32_t hi_mul = a.hi_mul;
 
     for (long long chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
         const long long tile = chunk * W + warp;
@@ -293,8 +324,8 @@ __global__ void __launch_bounds__(256) lb_kernel(const LbArgs a)
 #pragma unroll
             for (int k = 0; k < MAXM; ++k) {
                 if (k < m) {
-                    Rs[k * 64 + q * 32 + lane] = R[k];
-                    Ts[k * 64 + q * 32 + lane] = Q[k] + Ld[k];
+                    Rs[k * 64 + q * 32 + lane] = (rt_t)R[k];
+                    Ts[k * 64 + q * 32 + lane] = (rt_t)(Q[k] + Ld[k]);
                 }
             }
         }
@@ -333,19 +364,41 @@ __global__ void __launch_bounds__(256) lb_kernel(const LbArgs a)
                 // lines 08-17, software-pipelined 4 positions per step: records
                 // two steps ahead, U masks one step ahead (the group blob ends
                 // with padding records so the look-ahead stays in bounds).
-                uint4 ra = rp[0], rb = rp[1], na = rp[2], nb = rp[3];
-                uint2 ma = FSP_MASK(ra.y), mb = FSP_MASK(ra.w);
-                uint2 mc = FSP_MASK(rb.y), md = FSP_MASK(rb.w);
-                for (int it = 0; it < n4; ++it) {
-                    const uint4 fa = rp[2 * it + 4], fb = rp[2 * it + 5];
-                    const uint2 xa = FSP_MASK(na.y), xb = FSP_MASK(na.w);
-                    const uint2 xc = FSP_MASK(nb.y), xd = FSP_MASK(nb.w);
-                    FSP_UPD(ma, ra.x, ra.y);
-                    FSP_UPD(mb, ra.z, ra.w);
-                    FSP_UPD(mc, rb.x, rb.y);
-                    FSP_UPD(md, rb.z, rb.w);
-                    ra = na; rb = nb; na = fa; nb = fb;
-                    ma = xa; mb = xb; mc = xc; md = xd;
+                // X/Y register sets alternate so no copies are needed.
+                uint4 xa = rp[0], xb = rp[1]; // step 0
+                uint4 ya = rp[2], yb = rp[3]; // step 1
+                uint2 mx0 = FSP_MASK(xa.y), mx1 = FSP_MASK(xa.w);
+                uint2 mx2 = FSP_MASK(xb.y), mx3 = FSP_MASK(xb.w);
+                int s = 0;
+                for (; s + 2 <= n4; s += 2) {
+                    const uint2 my0 = FSP_MASK(ya.y), my1 = FSP_MASK(ya.w);
+                    const uint2 my2 = FSP_MASK(yb.y), my3 = FSP_MASK(yb.w);
+                    FSP_UPD(mx0, xa.x, xa.y);
+                    FSP_UPD(mx1, xa.z, xa.w);
+                    FSP_UPD(mx2, xb.x, xb.y);
+                    FSP_UPD(mx3, xb.z, xb.w);
+                    xa = rp[2 * s + 4];
+                    xb = rp[2 * s + 5];
+                    mx0 = FSP_MASK(xa.y);
+                    mx1 = FSP_MASK(xa.w);
+                    mx2 = FSP_MASK(xb.y);
+                    mx3 = FSP_MASK(xb.w);
+                    FSP_UPD(my0, ya.x, ya.y);
+                    FSP_UPD(my1, ya.z, ya.w);
+                    FSP_UPD(my2, yb.x, yb.y);
+                    FSP_UPD(my3, yb.z, yb.w);
+                    ya = rp[2 * s + 6];
+                    yb = rp[2 * s + 7];
+                }
+                if (s < n4) { // odd number of steps: the last one is in X
+                    FSP_UPD(mx0, xa.x, xa.y);
+                    FSP_UPD(mx1, xa.z, xa.w);
+                    FSP_UPD(mx2, xb.x, xb.y);
+                    FSP_UPD(mx3, xb.z, xb.w);
+                }
+                if constexpr (S16) {
+                    u0 = (int)(int16_t)(u0 & 0xffff);
+                    u1 = (int)(int16_t)(u1 & 0xffff);
                 }
                 lb0 = max(lb0, u0 + Ts[l * 64 + lane]); // lines 18-19
                 lb1 = max(lb1, u1 + Ts[l * 64 + 32 + lane]);
@@ -363,25 +416,25 @@ __global__ void smem_base_probe(uint32_t *out)
     *out = smem_u32(smem);
 }
 
-template <int MAXM, bool EXACT>
+template <int MAXM, bool EXACT, bool S16>
 int launch(const fsp_instance *inst, const LbArgs &a, cudaStream_t s)
 {
     const fsp_lb_plan &pl = inst->plan;
-    lb_kernel<MAXM, EXACT><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
+    lb_kernel<MAXM, EXACT, S16><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, "lb_kernel launch");
 }
 
-template <int MAXM, bool EXACT>
+template <int MAXM, bool EXACT, bool S16>
 int configure(fsp_instance *inst)
 {
     fsp_lb_plan &pl = inst->plan;
-    cudaError_t e = cudaFuncSetAttribute(lb_kernel<MAXM, EXACT>,
+    cudaError_t e = cudaFuncSetAttribute(lb_kernel<MAXM, EXACT, S16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)pl.smem_bytes);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "cudaFuncSetAttribute");
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM, EXACT>,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM, EXACT, S16>,
                                                       pl.warps * 32, pl.smem_bytes);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "occupancy");
     if (per_sm < 1) return fsp_fail(FSP_ERANGE, "lb kernel does not fit on an SM");
@@ -390,16 +443,22 @@ int configure(fsp_instance *inst)
     return FSP_OK;
 }
 
-// (MAXM, EXACT) specialisations: exact for Taillard's 5/10/20 machines.
-#define FSP_DISPATCH(FN, ...)                                                   \
+// (MAXM, EXACT, S16) specialisations: exact for Taillard's 5/10/20 machines.
+#define FSP_DISPATCH_M(FN, S, ...)                                              \
     switch (pl.maxm * 2 + (pl.exact ? 1 : 0)) {                                 \
-    case 5 * 2 + 1: return FN<5, true>(__VA_ARGS__);                            \
-    case 10 * 2 + 1: return FN<10, true>(__VA_ARGS__);                          \
-    case 20 * 2 + 1: return FN<20, true>(__VA_ARGS__);                          \
-    case 8 * 2: return FN<8, false>(__VA_ARGS__);                               \
-    case 16 * 2: return FN<16, false>(__VA_ARGS__);                             \
-    case 24 * 2: return FN<24, false>(__VA_ARGS__);                             \
-    default: return FN<32, false>(__VA_ARGS__);                                 \
+    case 5 * 2 + 1: return FN<5, true, S>(__VA_ARGS__);                         \
+    case 10 * 2 + 1: return FN<10, true, S>(__VA_ARGS__);                       \
+    case 20 * 2 + 1: return FN<20, true, S>(__VA_ARGS__);                       \
+    case 8 * 2: return FN<8, false, S>(__VA_ARGS__);                            \
+    case 16 * 2: return FN<16, false, S>(__VA_ARGS__);                          \
+    case 24 * 2: return FN<24, false, S>(__VA_ARGS__);                          \
+    default: return FN<32, false, S>(__VA_ARGS__);                              \
+    }
+#define FSP_DISPATCH(FN, ...)                                                   \
+    if (pl.s16) {                                                               \
+        FSP_DISPATCH_M(FN, true, __VA_ARGS__)                                   \
+    } else {                                                                    \
+        FSP_DISPATCH_M(FN, false, __VA_ARGS__)                                  \
     }
 
 } // namespace
@@ -429,6 +488,10 @@ int fsp_plan_lb(fsp_instance *inst)
     fsp_lb_plan &pl = inst->plan;
     const int n = inst->n, m = inst->m, P = inst->P;
     pl.exact = (m == 5 || m == 10 || m == 20);
+    // 16-bit walk when every walk value fits int16: t2 <= (n+m-1)*max p and
+    // w >= -n*max p
+    pl.s16 = (int64_t)(n + m - 1) * inst->max_p <= 32767 && (int64_t)n * inst->max_p <= 32767;
+    if (const char *s = getenv("FSP_LB_S16")) pl.s16 = pl.s16 && atoi(s) != 0;
     if (pl.exact) pl.maxm = m;
     else if (m <= 8) pl.maxm = 8;
     else if (m <= 16) pl.maxm = 16;
@@ -445,10 +508,16 @@ int fsp_plan_lb(fsp_instance *inst)
     pl.num_sms = sms;
     const int mp4 = (m + 3) & ~3;
     pl.nrec = (n + 3) & ~3; // walk steps of 4 positions
-    int want_warps = 8;
+    int want_warps = pl.s16 ? 16 : 8;
     if (const char *s = getenv("FSP_LB_WARPS")) want_warps = atoi(s);
     if (want_warps < 1) want_warps = 1;
-    if (want_warps > 8) want_warps = 8;
+    if (want_warps > 16) want_warps = 16;
+    if (pl.maxm > 20 && want_warps > 8) want_warps = 8; // launch bounds of the wide variants
+    // Score each feasible (W, G): more resident warps hide the walk's latency,
+    // each extra couple group costs one table reload per chunk (~1%).
+    double best = -1.0;
+    fsp_lb_layout bestL{};
+    int bestW = 0, bestG = 0, bestPPG = 0;
     for (int W = want_warps; W >= 1; --W) {
         fsp_lb_layout L{};
         L.u_bytes = align16((size_t)(n + 1) * 8 * W);
@@ -457,7 +526,7 @@ int fsp_plan_lb(fsp_instance *inst)
         L.ptm_bytes = align16((size_t)n * mp4 * 4);
         L.off_ptm = L.u_bytes;
         L.off_bar = L.off_ptm + L.ptm_bytes;
-        L.rt_bytes = 2 * (size_t)pl.maxm * 64 * 4;
+        L.rt_bytes = 2 * (size_t)pl.maxm * 64 * (pl.s16 ? 2 : 4);
         L.off_rt = L.off_bar + 16;
         L.off_tab = align16(L.off_rt + (size_t)W * L.rt_bytes);
         for (int G = 1; G <= P; ++G) {
@@ -468,16 +537,27 @@ int fsp_plan_lb(fsp_instance *inst)
             const size_t gb =
                 align16(L.kl_bytes + ((size_t)ppg * pl.nrec + FSP_REC_SLACK) * sizeof(fsp_rec));
             if (L.off_tab + gb <= (size_t)optin) {
-                L.group_bytes = gb;
-                pl.L = L;
-                pl.groups = Greal;
-                pl.pairs_per_group = ppg;
-                pl.warps = W;
-                pl.smem_bytes = L.off_tab + gb;
-                FSP_DISPATCH(configure, inst);
+                const double score = (double)W / (1.0 + 0.015 * (Greal - 1));
+                if (score > best) {
+                    best = score;
+                    L.group_bytes = gb;
+                    bestL = L;
+                    bestW = W;
+                    bestG = Greal;
+                    bestPPG = ppg;
+                }
+                break; // more groups only cost for this W
             }
             if (ppg == 1) break;
         }
+    }
+    if (best > 0) {
+        pl.L = bestL;
+        pl.groups = bestG;
+        pl.pairs_per_group = bestPPG;
+        pl.warps = bestW;
+        pl.smem_bytes = bestL.off_tab + bestL.group_bytes;
+        FSP_DISPATCH(configure, inst);
     }
     return fsp_fail(FSP_ERANGE, "instance tables do not fit in shared memory");
 }
@@ -504,5 +584,6 @@ int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stri
     a.mp4 = (inst->m + 3) & ~3;
     a.nrec = pl.nrec;
     a.stride = stride;
+    a.hi_mul = 0x10000u;
     FSP_DISPATCH(launch, inst, a, s);
 }

@@ -43,5 +43,5 @@ if __name__ == "__main__":
     cfgs = sys.argv[1:] or ["ta091"]
     for c in cfgs:
         name, N = (c.split(":") + ["1048576"])[:2]
-        for w in (8, 6, 4):
+        for w in ([int(x) for x in os.environ.get("SWEEP_WARPS", "16,8").split(",")]):
             print(json.dumps(time_cfg(name, int(N), w)), flush=True)
