@@ -147,9 +147,14 @@ int fsp_bb_solve(const fsp_instance *inst, int32_t initial_ub, int64_t max_nodes
  *                     descendants assigned to it).
  *  fsp_bb_step        up to `iters` expand/bound/prune iterations on stream;
  *                     synchronous (reads the pool size back).
- *  fsp_bb_ub_ptr      DEVICE int64 word = (incumbent << 32) | rank, for a
- *                     MIN all-reduce; after the collective call
- *                     fsp_bb_ub_sync to adopt the global incumbent.
+ *  fsp_bb_ub_publish  writes (best << 32) | rank into a caller DEVICE int64
+ *                     (stream-ordered), best = makespan of the schedule this
+ *                     rank holds (INT32_MAX: none): the operand of a MIN
+ *                     all-reduce, whose low 32 bits then name the holder;
+ *  fsp_bb_ub_adopt    incumbent <- min(incumbent, *d_src >> 32) on the device
+ *                     (after the collective); the permutation stays with the
+ *                     rank in the low 32 bits of the reduced word.
+ *  fsp_bb_ub_get/set  the same exchange through a HOST int64 (gloo, tests).
  *  fsp_bb_pool_size   HOST out: open nodes in the pool.
  *  fsp_bb_export      move up to max_nodes open nodes into a DEVICE buffer of
  *                     fsp_bb_node_bytes(state) bytes per node (donor side).
@@ -160,8 +165,10 @@ int fsp_bb_solve(const fsp_instance *inst, int32_t initial_ub, int64_t max_nodes
 int fsp_bb_init(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_t world,
                 void **state);
 int fsp_bb_step(void *state, int32_t iters, void *cuda_stream);
-int fsp_bb_ub_ptr(void *state, int64_t **d_packed_ub);
-int fsp_bb_ub_sync(void *state, void *cuda_stream);
+int fsp_bb_ub_publish(void *state, int64_t *d_dst, void *cuda_stream);
+int fsp_bb_ub_adopt(void *state, const int64_t *d_src, void *cuda_stream);
+int fsp_bb_ub_get(void *state, int64_t *packed);
+int fsp_bb_ub_set(void *state, int64_t packed);
 int fsp_bb_pool_size(void *state, int64_t *n);
 int64_t fsp_bb_node_bytes(void *state);
 int fsp_bb_export(void *state, int64_t max_nodes, void *d_buf, int64_t *n_out);

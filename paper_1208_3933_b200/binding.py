@@ -24,7 +24,8 @@ _NAMES = {0: "FSP_OK", -1: "FSP_EINVAL", -2: "FSP_ERANGE", -3: "FSP_ENOMEM", -4:
 EXPORTS = [
     "fsp_instance_load", "fsp_instance_free", "fsp_instance_get_info", "fsp_lb_eval",
     "fsp_lb_eval_host", "fsp_check", "fsp_lb_work", "fsp_bb_solve", "fsp_bb_init",
-    "fsp_bb_step", "fsp_bb_ub_ptr", "fsp_bb_ub_sync", "fsp_bb_pool_size", "fsp_bb_node_bytes",
+    "fsp_bb_step", "fsp_bb_ub_publish", "fsp_bb_ub_adopt", "fsp_bb_ub_get", "fsp_bb_ub_set",
+    "fsp_bb_pool_size", "fsp_bb_node_bytes",
     "fsp_bb_export", "fsp_bb_import", "fsp_bb_result", "fsp_bb_get_stats", "fsp_bb_free",
     "fsp_last_error", "fsp_version",
 ]
@@ -71,8 +72,10 @@ def lib():
                                        C.POINTER(BBStats)]),
             "fsp_bb_init": (C.c_int, [vp, i32, i32, i32, C.POINTER(vp)]),
             "fsp_bb_step": (C.c_int, [vp, i32, vp]),
-            "fsp_bb_ub_ptr": (C.c_int, [vp, C.POINTER(vp)]),
-            "fsp_bb_ub_sync": (C.c_int, [vp, vp]),
+            "fsp_bb_ub_publish": (C.c_int, [vp, vp, vp]),
+            "fsp_bb_ub_adopt": (C.c_int, [vp, vp, vp]),
+            "fsp_bb_ub_get": (C.c_int, [vp, C.POINTER(i64)]),
+            "fsp_bb_ub_set": (C.c_int, [vp, i64]),
             "fsp_bb_pool_size": (C.c_int, [vp, C.POINTER(i64)]),
             "fsp_bb_node_bytes": (i64, [vp]),
             "fsp_bb_export": (C.c_int, [vp, i64, vp, C.POINTER(i64)]),
@@ -188,3 +191,71 @@ class Instance:
                                 C.byref(ms), perm.ctypes.data, C.byref(st))
         _check(rc, allow=(FSP_ENOTFOUND, FSP_EBUDGET))
         return rc, int(ms.value), perm, {f: getattr(st, f) for f, _ in BBStats._fields_}
+
+
+class BBState:
+    """Step-level device B&B (fsp_bb_init / fsp_bb_step / ...) for one rank."""
+
+    def __init__(self, inst: Instance, initial_ub: int = 2**31 - 1, rank: int = 0, world: int = 1):
+        self.inst = inst
+        self.n = inst.n
+        h = C.c_void_p()
+        _check(lib().fsp_bb_init(inst._h, int(initial_ub), int(rank), int(world), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().fsp_bb_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, iters: int = 1):
+        _check(lib().fsp_bb_step(self._h, int(iters), None))
+
+    def pool_size(self) -> int:
+        v = C.c_int64(0)
+        _check(lib().fsp_bb_pool_size(self._h, C.byref(v)))
+        return int(v.value)
+
+    def ub_publish(self, d_word) -> None:
+        """(incumbent << 32) | rank -> a torch int64 CUDA tensor of one element."""
+        _check(lib().fsp_bb_ub_publish(self._h, _ptr(d_word), _stream(None)))
+
+    def ub_adopt(self, d_word) -> None:
+        _check(lib().fsp_bb_ub_adopt(self._h, _ptr(d_word), _stream(None)))
+
+    def ub_get(self) -> int:
+        v = C.c_int64(0)
+        _check(lib().fsp_bb_ub_get(self._h, C.byref(v)))
+        return int(v.value)
+
+    def ub_set(self, packed: int) -> None:
+        _check(lib().fsp_bb_ub_set(self._h, int(packed)))
+
+    def node_bytes(self) -> int:
+        return int(lib().fsp_bb_node_bytes(self._h))
+
+    def export(self, max_nodes: int, d_buf_ptr: int) -> int:
+        k = C.c_int64(0)
+        _check(lib().fsp_bb_export(self._h, int(max_nodes), C.c_void_p(d_buf_ptr), C.byref(k)))
+        return int(k.value)
+
+    def import_(self, d_buf_ptr: int, k: int):
+        _check(lib().fsp_bb_import(self._h, C.c_void_p(d_buf_ptr), int(k)))
+
+    def result(self):
+        ms = C.c_int32(0)
+        perm = np.zeros(self.n, np.int32)
+        rc = _check(lib().fsp_bb_result(self._h, C.byref(ms), perm.ctypes.data),
+                    allow=(FSP_ENOTFOUND,))
+        return rc, int(ms.value), perm
+
+    def stats(self) -> dict:
+        st = BBStats()
+        _check(lib().fsp_bb_get_stats(self._h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in BBStats._fields_}

@@ -100,6 +100,7 @@ struct LbArgs {
     int32_t *lb_out;
     int *err;
     long long pool;
+    const long long *pool_dev; // if set, the pool size is read on the device (B&B)
     uint32_t smem_base;    // shared-window address the host baked into the records
     fsp_lb_layout L;
     int groups, ppg;       // couple groups, couples per group
@@ -197,7 +198,8 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs 
     phase ^= 1;
     int resident = 0;
 
-    const long long ntiles = (a.pool + 63) >> 6;
+    const long long pool = a.pool_dev ? *a.pool_dev : a.pool;
+    const long long ntiles = (pool + 63) >> 6;
     const long long nchunks = (ntiles + W - 1) / W;
     const uint32_t lanebit = 1u << lane;
     const uint32_t w8 = 8u * warp;
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs 
     for (long long chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
         const long long tile = chunk * W + warp;
         const long long node0 = tile * 64 + lane, node1 = node0 + 32;
-        const bool has0 = node0 < a.pool, has1 = node1 < a.pool;
+        const bool has0 = node0 < pool, has1 = node1 < pool;
         bool bad = false;
 
         // ---------------- a1: node ingest (depth, scheduled set) ----------------
@@ -565,6 +567,13 @@ int fsp_plan_lb(fsp_instance *inst)
 int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                   const int32_t *depth, int64_t pool, int32_t *lb_out, cudaStream_t s)
 {
+    return fsp_launch_lb_dev(inst, prefix, stride, depth, pool, nullptr, lb_out, s);
+}
+
+int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
+                      const int32_t *depth, int64_t pool, const int64_t *pool_dev,
+                      int32_t *lb_out, cudaStream_t s)
+{
     const fsp_lb_plan &pl = inst->plan;
     LbArgs a;
     a.tables = inst->d_tables;
@@ -574,6 +583,7 @@ int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stri
     a.lb_out = lb_out;
     a.err = inst->d_err;
     a.pool = pool;
+    a.pool_dev = reinterpret_cast<const long long *>(pool_dev);
     a.smem_base = pl.smem_base;
     a.L = pl.L;
     a.groups = pl.groups;

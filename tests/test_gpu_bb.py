@@ -1,0 +1,154 @@
+"""GPU parity of the device B&B (fsp_bb_solve / step API) against the oracle.
+
+The optimum is unique, the permutation is not: checks are makespan(perm) ==
+returned makespan == oracle / brute-force optimum."""
+import itertools
+
+import numpy as np
+import pytest
+
+from paper_1208_3933_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fsp():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1208_3933_b200 import binding
+    binding.lib()
+    return binding
+
+
+def brute(p):
+    n = p.shape[0]
+    best = None
+    for q in itertools.permutations(range(n)):
+        m = p.shape[1]
+        C = [0] * m
+        for j in q:
+            prev = 0
+            for k in range(m):
+                C[k] = max(C[k], prev) + int(p[j, k])
+                prev = C[k]
+        best = C[-1] if best is None else min(best, C[-1])
+    return best
+
+
+def test_bb_bruteforce(fsp, orc):
+    rng = np.random.default_rng(31)
+    for _ in range(40):
+        n, m = int(rng.integers(1, 8)), int(rng.integers(2, 6))
+        p = rng.integers(1, 40, (n, m)).astype(np.int32)
+        opt = brute(p)
+        inst = fsp.Instance(p)
+        rc, ms, perm, st = inst.bb_solve()
+        assert rc == 0 and ms == opt, (p.tolist(), ms, opt)
+        assert orc.makespan(p, perm) == opt and sorted(perm.tolist()) == list(range(n))
+        rc, ms, perm, _ = inst.bb_solve(opt)             # UB equal to the optimum: found (R9)
+        assert rc == 0 and ms == opt
+        if opt > 0:
+            rc, ms, _, _ = inst.bb_solve(opt - 1)         # below it: none
+            assert rc == fsp.FSP_ENOTFOUND
+
+
+def test_bb_matches_oracle_medium(fsp, orc):
+    rng = np.random.default_rng(77)
+    for _ in range(6):
+        n, m = int(rng.integers(9, 13)), int(rng.integers(3, 6))
+        p = rng.integers(1, 99, (n, m)).astype(np.int32)
+        orc_rc, orc_ms, _, _ = orc.Tables(p).bb_dfs()
+        rc, ms, perm, st = fsp.Instance(p).bb_solve()
+        assert rc == 0 and orc_rc == 0 and ms == orc_ms
+        assert orc.makespan(p, perm) == ms
+
+
+def test_bb_m2_johnson(fsp, orc):
+    rng = np.random.default_rng(5)
+    for _ in range(5):
+        n = int(rng.integers(5, 60))
+        p = rng.integers(1, 99, (n, 2)).astype(np.int32)
+        order = orc.johnson_order(p[:, 0], p[:, 1])
+        rc, ms, perm, _ = fsp.Instance(p).bb_solve()
+        assert rc == 0 and ms == orc.makespan(p, order) == orc.makespan(p, perm)
+
+
+def test_bb_ta002(fsp, orc):
+    p = inputs.instance("ta002")
+    rc, ms, perm, st = fsp.Instance(p).bb_solve()
+    assert rc == 0 and ms == 1359 and orc.makespan(p, perm) == 1359
+
+
+def test_bb_budget(fsp, orc):
+    p = inputs.instance("ta021")
+    rc, ms, perm, st = fsp.Instance(p).bb_solve(2**31 - 1, 200000, 0.0)
+    assert rc in (fsp.FSP_EBUDGET, fsp.FSP_ENOTFOUND)
+    assert st["bounded"] >= 200000
+    if rc == fsp.FSP_EBUDGET:
+        assert orc.makespan(p, perm) == ms
+
+
+def test_bb_two_ranks_one_gpu(fsp, orc):
+    """The step API with world=2 on one device: host-side MIN of the packed
+    incumbents stands in for the NCCL all-reduce; the optimum must equal the
+    single-rank one; export/import move open nodes between the ranks."""
+    import torch
+    rng = np.random.default_rng(12)
+    for _ in range(4):
+        n, m = int(rng.integers(6, 11)), int(rng.integers(3, 6))
+        p = rng.integers(1, 60, (n, m)).astype(np.int32)
+        opt = orc.Tables(p).bb_dfs()[1]
+        inst = fsp.Instance(p)
+        ranks = [fsp.BBState(inst, 2**31 - 1, r, 2) for r in range(2)]
+        buf = torch.empty(4096 * ranks[0].node_bytes(), dtype=torch.uint8, device="cuda")
+        for it in range(100000):
+            for s in ranks:
+                s.step(2)
+            g = min(s.ub_get() for s in ranks)       # the MIN all-reduce, on the host
+            for s in ranks:
+                s.ub_set(g)
+            sizes = [s.pool_size() for s in ranks]
+            if sum(sizes) == 0:
+                break
+            # rebalance: the larger pool donates half of the difference
+            a, b = (0, 1) if sizes[0] >= sizes[1] else (1, 0)
+            give = min((sizes[a] - sizes[b]) // 2, 4096)
+            if give > 0:
+                k = ranks[a].export(give, buf.data_ptr())
+                ranks[b].import_(buf.data_ptr(), k)
+        results = [s.result() for s in ranks]
+        best = min(r[1] for r in results if r[0] == 0)
+        assert best == opt
+        for rc, ms, perm in results:
+            if rc == 0:
+                assert orc.makespan(p, perm) == ms
+
+
+def test_distributed_driver_nccl_world1(fsp, orc):
+    """dist.distributed_bb over a real NCCL process group (world 1) with the
+    device engine: the adapter path bench.py uses on N GPUs."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1208_3933_b200 import dist as fdist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(3)
+        p = rng.integers(1, 60, (9, 4)).astype(np.int32)
+        opt = orc.Tables(p).bb_dfs()[1]
+        inst = fsp.Instance(p)
+        eng = fdist.DeviceEngine(fsp.BBState(inst, 2**31 - 1, 0, 1), "cuda")
+        res = fdist.distributed_bb(eng, dist, rank=0, world=1, device="cuda", sync_every=2)
+        assert res.status == 0 and res.makespan == opt
+        assert orc.makespan(p, res.perm) == opt
+    finally:
+        dist.destroy_process_group()

@@ -1,6 +1,5 @@
 set -x
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -30 > gpurun_out/pytest_gpu.txt
 cat gpurun_out/pytest_gpu.txt
-timeout 600 python tools/lb_sweep.py ta091:1048576 ta021:1048576 ta051:1048576 ta111:262144 > gpurun_out/sweep.txt 2>&1; cat gpurun_out/sweep.txt
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:lb_kernel -s 3 -c 1 -o gpurun_out/prof_lb4 python bench.py --steps 1 --warmup 3 --no-bb --no-e2e --cpu-seconds 1 > gpurun_out/ncu4.log 2>&1
-tail -1 gpurun_out/ncu4.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; tail -3 gpurun_out/smoke.txt
+timeout 600 python tools/bb_try.py ta002:2147483647:30 ta001:1278:60 ta001:2147483647:30 ta091:2147483647:20 > gpurun_out/bb_try.txt 2>&1; cat gpurun_out/bb_try.txt
