@@ -342,23 +342,30 @@ int bb_iterate(BBState *s)
     // exact child count is checked after the scan and B halved if it overflows
     const double kpp = std::max(1.0, std::min((double)n, s->kids_per_parent));
     int64_t B = std::min<int64_t>(open, std::max<int64_t>(1, (int64_t)(s->ccap / kpp)));
+    // beam width of the depth-first batches: B parents per level with ~n/2
+    // children each over n levels must fit the stack (B * n^2/2 <= cap)
+    B = std::min<int64_t>(B, std::max<int64_t>(1, s->cap / std::max<int64_t>(1, (int64_t)n * n / 2)));
+    // keep n*n slots of headroom: from any state a depth-first descent (B = 1)
+    // needs at most n children per level for n levels, so the search never
+    // dead-ends on memory
+    const int64_t usable = s->cap - (int64_t)n * n;
     int64_t first = 0;
     for (;;) {
-        while (B > 1 && (s->size - B) + B * n > s->cap) B = (B + 1) / 2;
-        if ((s->size - B) + B * n > s->cap) return fsp_fail(FSP_ENOMEM, "B&B stack full");
         first = s->size - B;
         scan_kernel<<<1, kScanThreads, 0, st>>>(0, s->st_dp + first, n, nullptr, nullptr, B, s->off);
-        long long C = 0;
         cudaError_t e = cudaMemcpyAsync(&s->h_status->children, s->off + B, 8,
                                         cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return fsp_cuda_fail(e, "B&B scan");
-        C = s->h_status->children;
-        if (C <= s->ccap || B == 1) {
-            if (C > s->ccap) return fsp_fail(FSP_ENOMEM, "B&B child buffer too small");
+        const long long C = s->h_status->children;
+        // the children must fit the child buffer, and (all surviving) the stack
+        const int64_t room = std::max<int64_t>(0, std::min<int64_t>(s->ccap, usable - first));
+        if (C <= room) break;
+        if (B == 1) {
+            if (first + C > s->cap || C > s->ccap) return fsp_fail(FSP_ENOMEM, "B&B stack full");
             break;
         }
-        B = std::max<int64_t>(1, (int64_t)((double)B * s->ccap / (double)C * 0.9));
+        B = std::max<int64_t>(1, std::min<int64_t>(B / 2, (int64_t)((double)B * room / (double)C * 0.9)));
     }
     s->size = first;
     const int64_t maxC = s->h_status->children;
@@ -423,10 +430,12 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     // child buffer: enough children to fill the GPU several times over
     s->ccap = env_i64("FSP_BB_CHILDREN", std::max<int64_t>(1 << 22, (int64_t)n * 4));
     s->kids_per_parent = n;
-    const double frac = 0.25;
+    // the stack may take most of the free HBM (180 GB per B200): its size bounds
+    // the beam width of the depth-first batches (see bb_iterate)
+    const double frac = getenv("FSP_BB_MEM_FRAC") ? atof(getenv("FSP_BB_MEM_FRAC")) : 0.6;
     int64_t cap = (int64_t)((double)freeb * frac / rec);
     cap = env_i64("FSP_BB_STACK", std::min<int64_t>(cap, (int64_t)1 << 31));
-    s->cap = std::max<int64_t>(cap, (int64_t)n * 4);
+    s->cap = std::max<int64_t>(cap, (int64_t)n * n * 4);
     const int64_t maxB = s->ccap; // parents per iteration never exceed the children
     const int64_t nblk = (s->ccap + kPruneThreads - 1) / kPruneThreads + 1;
     auto alloc = [&](void **p, size_t bytes) {
