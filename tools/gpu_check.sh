@@ -1,3 +1,5 @@
 set -x
-timeout 600 python tools/bb_try.py ta091:2147483647:20 ta051:2147483647:20 ta021:2147483647:20 > gpurun_out/bb_try.txt 2>&1; cat gpurun_out/bb_try.txt
-FSP_BB_STACK=200000 timeout 600 python tools/bb_try.py ta091:2147483647:10 > gpurun_out/bb_try2.txt 2>&1; cat gpurun_out/bb_try2.txt
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 5 --warmup 3 --no-bb --no-e2e --cpu-seconds 1 > gpurun_out/ncu_launch_bench.log 2>&1
+tail -2 gpurun_out/ncu_launch_bench.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 2000 -c 600 --csv --log-file gpurun_out/launches_bb.csv python tools/bb_try.py ta091:2147483647:20 > gpurun_out/ncu_launch_bb.log 2>&1
+tail -2 gpurun_out/ncu_launch_bb.log
