@@ -24,10 +24,10 @@ struct __align__(8) fsp_rec {
 
 // Dynamic shared-memory layout of the lb kernel (byte offsets).
 struct fsp_lb_layout {
-    size_t off_u, u_bytes;     // U[(n+1)][W] uint2 transposed unscheduled sets
+    size_t off_u, u_bytes;     // U[(n+1)][W][npl] u32 transposed unscheduled sets
     size_t off_ptm, ptm_bytes; // PTM int32 [n][mp4]
     size_t off_bar;            // mbarrier
-    size_t off_rt, rt_bytes;   // per warp: R[MAXM][64], T[MAXM][64] int32
+    size_t off_rt, rt_bytes;   // per warp: R[MAXM][32*npl], T[MAXM][32*npl]
     size_t off_tab;            // one couple group: [kl header][records]
     size_t kl_bytes, group_bytes;
 };
@@ -36,6 +36,7 @@ struct fsp_lb_plan {
     int maxm;            // machine-count specialisation (template)
     bool exact;          // maxm == m (5, 10, 20)
     bool s16;            // 16-bit walk (records in the s16 meta form)
+    int npl;             // nodes per lane (2 or 4): U rows are 4*npl bytes per warp
     uint32_t smem_base;  // shared-window address of dynamic smem offset 0
     int nrec;            // records per couple (n rounded up to even)
     fsp_lb_layout L;
@@ -44,6 +45,7 @@ struct fsp_lb_plan {
     int warps;           // warps per CTA
     int ctas_per_sm;
     int num_sms;
+    int smem_optin;      // cudaDevAttrMaxSharedMemoryPerBlockOptin
     int grid;
     size_t smem_bytes;   // dynamic smem per CTA
 };

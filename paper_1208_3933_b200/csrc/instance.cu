@@ -71,7 +71,7 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
     const size_t kl_bytes = pl.L.kl_bytes;
     // shared address of U[j][warp 0]; row n is the always-empty padding row
     auto uaddr = [&](int j) {
-        return (uint32_t)(pl.smem_base + pl.L.off_u + (size_t)j * 8 * pl.warps);
+        return (uint32_t)(pl.smem_base + pl.L.off_u + (size_t)j * 4 * pl.npl * pl.warps);
     };
     std::vector<uint8_t> blob(gbytes * pl.groups, 0);
     for (int g = 0; g < pl.groups; ++g) { // every record slot starts as padding

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <type_traits>
@@ -85,13 +86,6 @@ __device__ __forceinline__ void bulk_copy(void *dst, const void *src, uint32_t b
     }
 }
 
-__device__ __forceinline__ uint2 lds_u2(uint32_t addr)
-{
-    uint2 v;
-    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
-    return v;
-}
-
 struct LbArgs {
     const uint8_t *tables; // groups x group_bytes
     const int32_t *ptm;    // [n][mp4] int32, ptm_bytes
@@ -109,17 +103,38 @@ struct LbArgs {
     uint32_t hi_mul;       // 0x10000 (see mask_addr)
 };
 
-// Shared address of U[job][warp] from a record's meta word.
-//   int32 form: meta = (c2 << 16) | addr    -> (meta & 0xffff) | 8*warp  (one LOP3)
-//   s16 form:   meta = (addr << 16) | c2    -> (meta >> 16) + 8*warp     (one IMAD.HI)
+// Shared address of U[job][warp] from a record's meta word (wst = 4*NPL*warp).
+//   int32 form: meta = (c2 << 16) | addr    -> (meta & 0xffff) | wst  (one LOP3)
+//   s16 form:   meta = (addr << 16) | c2    -> (meta >> 16) + wst     (one IMAD.HI)
 // (hi_mul = 0x10000 arrives as a kernel argument so ptxas keeps an IMAD.HI on
 // the FMA pipe instead of strength-reducing it to an ALU LEA.HI: the ALU pipe
 // is the walk's bottleneck.)
 template <bool S16>
-__device__ __forceinline__ uint32_t mask_addr(uint32_t meta, uint32_t w8, uint32_t hi_mul)
+__device__ __forceinline__ uint32_t mask_addr(uint32_t meta, uint32_t wst, uint32_t hi_mul)
 {
-    if constexpr (S16) return __umulhi(meta, hi_mul) + w8;
-    else return (meta & 0xffffu) | w8;
+    if constexpr (S16) return __umulhi(meta, hi_mul) + wst;
+    else return (meta & 0xffffu) | wst;
+}
+
+// The NPL unscheduled-bit words of one job for this warp's NPL*32 nodes.
+template <int NPL>
+struct Mask {
+    uint32_t b[NPL];
+};
+
+template <int NPL>
+__device__ __forceinline__ Mask<NPL> lds_mask(uint32_t addr)
+{
+    Mask<NPL> v;
+    if constexpr (NPL == 2) {
+        asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.b[0]), "=r"(v.b[1]) : "r"(addr));
+    } else {
+        static_assert(NPL == 4, "NPL is 2 or 4");
+        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+            : "=r"(v.b[0]), "=r"(v.b[1]), "=r"(v.b[2]), "=r"(v.b[3])
+            : "r"(addr));
+    }
+    return v;
 }
 
 // One update of Fig. 3 lines 10-15 in the (u, w) form for one node; line 10
@@ -144,29 +159,30 @@ __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1
     }
 }
 
-#define FSP_MASK(META) lds_u2(mask_addr<S16>((META), w8, hi_mul))
+#define FSP_MASK(META) lds_mask<NPL>(mask_addr<S16>((META), wst, hi_mul))
 #define FSP_UPD(MASK, C1, META)                                                 \
     {                                                                           \
-        upd<S16>((MASK).x, lanebit, (C1), (META), u0, w0);                      \
-        upd<S16>((MASK).y, lanebit, (C1), (META), u1, w1);                      \
+        _Pragma("unroll") for (int q_ = 0; q_ < NPL; ++q_)                      \
+            upd<S16>((MASK).b[q_], lanebit, (C1), (META), uu[q_], ww[q_]);      \
     }
 
-template <int MAXM, bool EXACT, bool S16>
-__global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs a)
+template <int MAXM, bool EXACT, bool S16, int NPL>
+__global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbArgs a)
 {
     extern __shared__ __align__(128) uint8_t smem[];
     const int n = a.n;
     const int m = EXACT ? MAXM : a.m;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int W = blockDim.x >> 5;
-    uint32_t *Uw = reinterpret_cast<uint32_t *>(smem + a.L.off_u);      // [(n+1)][W][2]
+    constexpr int TN = 32 * NPL;                                         // nodes per warp
+    uint32_t *Uw = reinterpret_cast<uint32_t *>(smem + a.L.off_u);      // [(n+1)][W][NPL]
     const int32_t *s_ptm = reinterpret_cast<const int32_t *>(smem + a.L.off_ptm);
     uint64_t *s_bar = reinterpret_cast<uint64_t *>(smem + a.L.off_bar);
-    // per-warp heads R[MAXM][64] and tail+load T[MAXM][64]; int16 in the s16
+    // per-warp heads R[MAXM][TN] and tail+load T[MAXM][TN]; int16 in the s16
     // walk (all values fit, host-checked), int32 otherwise
     using rt_t = typename std::conditional<S16, int16_t, int32_t>::type;
     rt_t *Rs = reinterpret_cast<rt_t *>(smem + a.L.off_rt + (size_t)warp * a.L.rt_bytes);
-    rt_t *Ts = Rs + MAXM * 64;
+    rt_t *Ts = Rs + MAXM * TN;
     uint8_t *s_tab = smem + a.L.off_tab;
 
     if (smem_u32(smem) != a.smem_base) { // records carry absolute shared addresses
@@ -199,49 +215,64 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs 
     int resident = 0;
 
     const long long pool = a.pool_dev ? *a.pool_dev : a.pool;
-    const long long ntiles = (pool + 63) >> 6;
+    const long long ntiles = (pool + TN - 1) / TN;
     const long long nchunks = (ntiles + W - 1) / W;
     const uint32_t lanebit = 1u << lane;
-    const uint32_t w8 = 8u * warp;
+    const uint32_t wst = 4u * NPL * warp;
     const uint32_t hi_mul = a.hi_mul;
 
     for (long long chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
         const long long tile = chunk * W + warp;
-        const long long node0 = tile * 64 + lane, node1 = node0 + 32;
-        const bool has0 = node0 < pool, has1 = node1 < pool;
         bool bad = false;
 
         // ---------------- a1: node ingest (depth, scheduled set) ----------------
-        int d0 = 0, d1 = 0;
-        if (has0) d0 = a.depth[node0];
-        if (has1) d1 = a.depth[node1];
-        if (d0 < 0 || d0 > n || d0 > a.stride) { bad = true; d0 = 0; }
-        if (d1 < 0 || d1 > n || d1 > a.stride) { bad = true; d1 = 0; }
-        const uint32_t valid0 = __ballot_sync(0xffffffffu, has0);
-        const uint32_t valid1 = __ballot_sync(0xffffffffu, has1);
+        // lane `lane` owns nodes tile*TN + q*32 + lane, q < NPL
+        int dq[NPL];
+        uint32_t validq[NPL];
+        uint32_t anyvalid = 0;
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const long long node = tile * TN + q * 32 + lane;
+            const bool has = node < pool;
+            int d = has ? a.depth[node] : 0;
+            if (d < 0 || d > n || d > a.stride) {
+                bad = true;
+                d = 0;
+            }
+            dq[q] = d;
+            validq[q] = __ballot_sync(0xffffffffu, has);
+            anyvalid |= validq[q];
+        }
         for (int j = lane; j <= n; j += 32) {
-            Uw[(j * W + warp) * 2 + 0] = j < n ? valid0 : 0u; // row n: the padding record's
-            Uw[(j * W + warp) * 2 + 1] = j < n ? valid1 : 0u; // always-empty mask
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) // row n: the padding record's always-empty mask
+                Uw[(j * W + warp) * NPL + q] = j < n ? validq[q] : 0u;
         }
         __syncwarp();
-        // coalesced pass over the 64 prefix records: clear the scheduled bits
-        for (int L = 0; L < 64; ++L) {
-            const int dL = __shfl_sync(0xffffffffu, L < 32 ? d0 : d1, L & 31);
-            if (dL == 0) continue;
-            const uint16_t *row = a.prefix + (size_t)(tile * 64 + L) * a.stride;
-            const uint32_t clr = ~(1u << (L & 31));
-            for (int i = lane; i < dL; i += 32) {
-                const uint32_t job = row[i];
-                if (job < (uint32_t)n) Uw[(job * W + warp) * 2 + (L >> 5)] &= clr;
+        // coalesced pass over the TN prefix records: clear the scheduled bits
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            for (int L = 0; L < 32; ++L) {
+                const int dL = __shfl_sync(0xffffffffu, dq[q], L);
+                if (dL == 0) continue;
+                const uint16_t *row = a.prefix + (size_t)(tile * TN + q * 32 + L) * a.stride;
+                const uint32_t clr = ~(1u << L);
+                for (int i = lane; i < dL; i += 32) {
+                    const uint32_t job = row[i];
+                    if (job < (uint32_t)n) Uw[(job * W + warp) * NPL + q] &= clr;
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
 
         // ---------------- per node of this lane: C, heads, tails ----------------
 #pragma unroll 1
-        for (int q = 0; q < 2; ++q) {
-            const long long node = q ? node1 : node0;
-            const int d = q ? d1 : d0;
+        for (int q = 0; q < NPL; ++q) {
+            const long long node = tile * TN + q * 32 + lane;
+            int d = dq[0]; // (select chain: no local-memory indexing)
+#pragma unroll
+            for (int t = 1; t < NPL; ++t)
+                if (q == t) d = dq[t];
             // prefix completion times C_k
             int C[MAXM];
 #pragma unroll
@@ -280,7 +311,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs 
             }
             int cnt = 0;
             for (int j = 0; j < n; ++j) {
-                const uint32_t uj = Uw[(j * W + warp) * 2 + q];
+                const uint32_t uj = Uw[(j * W + warp) * NPL + q];
                 if (uj == 0) continue; // scheduled in every node of this half-warp
                 if (uj & lanebit) {
                     ++cnt;
@@ -314,7 +345,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs 
                     }
                 }
             }
-            if ((q ? has1 : has0) && cnt != n - d) bad = true; // repeated / bad job
+            if (node < pool && cnt != n - d) bad = true; // repeated / bad job
             if (cnt == 0) { // R6: complete schedule
 #pragma unroll
                 for (int k = 0; k < MAXM; ++k) {
@@ -326,8 +357,8 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs 
 #pragma unroll
             for (int k = 0; k < MAXM; ++k) {
                 if (k < m) {
-                    Rs[k * 64 + q * 32 + lane] = (rt_t)R[k];
-                    Ts[k * 64 + q * 32 + lane] = (rt_t)(Q[k] + Ld[k]);
+                    Rs[k * TN + q * 32 + lane] = (rt_t)R[k];
+                    Ts[k * TN + q * 32 + lane] = (rt_t)(Q[k] + Ld[k]);
                 }
             }
         }
@@ -335,7 +366,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs 
         __syncwarp();
 
         // ---------------- a4/a5: couple walks (Fig. 3 lines 03-19) ----------------
-        int lb0 = 0, lb1 = 0; // R1
+        int lb[NPL]; // R1: the max over couples starts at 0
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) lb[q] = 0;
         const bool ascending = resident == 0;
         for (int gi = 0; gi < a.groups; ++gi) {
             const int g = ascending ? gi : a.groups - 1 - gi;
@@ -351,7 +384,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs 
                 phase ^= 1;
                 resident = g;
             }
-            if ((valid0 | valid1) == 0) continue;
+            if (anyvalid == 0) continue;
             const uint32_t *kl = reinterpret_cast<const uint32_t *>(s_tab);
             const uint4 *recs = reinterpret_cast<const uint4 *>(s_tab + a.L.kl_bytes);
             const int np = group_size(g);
@@ -360,8 +393,12 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs 
                 const uint32_t kv = kl[pl];
                 const int k = kv & 0xffff, l = kv >> 16;
                 // lines 06-07: timeOnM1 / timeOnM2 start at the RM minima
-                int u0 = Rs[l * 64 + lane], u1 = Rs[l * 64 + 32 + lane];
-                int w0 = Rs[k * 64 + lane], w1 = Rs[k * 64 + 32 + lane];
+                int uu[NPL], ww[NPL];
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) {
+                    uu[q] = Rs[l * TN + q * 32 + lane];
+                    ww[q] = Rs[k * TN + q * 32 + lane];
+                }
                 const uint4 *rp = recs + (size_t)pl * n2;
                 // lines 08-17, software-pipelined 4 positions per step: records
                 // two steps ahead, U masks one step ahead (the group blob ends
@@ -369,12 +406,12 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs 
                 // X/Y register sets alternate so no copies are needed.
                 uint4 xa = rp[0], xb = rp[1]; // step 0
                 uint4 ya = rp[2], yb = rp[3]; // step 1
-                uint2 mx0 = FSP_MASK(xa.y), mx1 = FSP_MASK(xa.w);
-                uint2 mx2 = FSP_MASK(xb.y), mx3 = FSP_MASK(xb.w);
+                Mask<NPL> mx0 = FSP_MASK(xa.y), mx1 = FSP_MASK(xa.w);
+                Mask<NPL> mx2 = FSP_MASK(xb.y), mx3 = FSP_MASK(xb.w);
                 int s = 0;
                 for (; s + 2 <= n4; s += 2) {
-                    const uint2 my0 = FSP_MASK(ya.y), my1 = FSP_MASK(ya.w);
-                    const uint2 my2 = FSP_MASK(yb.y), my3 = FSP_MASK(yb.w);
+                    const Mask<NPL> my0 = FSP_MASK(ya.y), my1 = FSP_MASK(ya.w);
+                    const Mask<NPL> my2 = FSP_MASK(yb.y), my3 = FSP_MASK(yb.w);
                     FSP_UPD(mx0, xa.x, xa.y);
                     FSP_UPD(mx1, xa.z, xa.w);
                     FSP_UPD(mx2, xb.x, xb.y);
@@ -399,15 +436,19 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512) lb_kernel(const LbArgs 
                     FSP_UPD(mx3, xb.z, xb.w);
                 }
                 if constexpr (S16) {
-                    u0 = (int)(int16_t)(u0 & 0xffff);
-                    u1 = (int)(int16_t)(u1 & 0xffff);
+#pragma unroll
+                    for (int q = 0; q < NPL; ++q) uu[q] = (int)(int16_t)(uu[q] & 0xffff);
                 }
-                lb0 = max(lb0, u0 + Ts[l * 64 + lane]); // lines 18-19
-                lb1 = max(lb1, u1 + Ts[l * 64 + 32 + lane]);
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) // lines 18-19
+                    lb[q] = max(lb[q], uu[q] + Ts[l * TN + q * 32 + lane]);
             }
         }
-        if (has0) a.lb_out[node0] = lb0;
-        if (has1) a.lb_out[node1] = lb1;
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const long long node = tile * TN + q * 32 + lane;
+            if (node < pool) a.lb_out[node] = lb[q];
+        }
         __syncwarp();
     }
 }
@@ -418,25 +459,27 @@ __global__ void smem_base_probe(uint32_t *out)
     *out = smem_u32(smem);
 }
 
-template <int MAXM, bool EXACT, bool S16>
+template <int MAXM, bool EXACT, bool S16, int NPL>
 int launch(const fsp_instance *inst, const LbArgs &a, cudaStream_t s)
 {
     const fsp_lb_plan &pl = inst->plan;
-    lb_kernel<MAXM, EXACT, S16><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
+    lb_kernel<MAXM, EXACT, S16, NPL><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, "lb_kernel launch");
 }
 
-template <int MAXM, bool EXACT, bool S16>
+template <int MAXM, bool EXACT, bool S16, int NPL>
 int configure(fsp_instance *inst)
 {
     fsp_lb_plan &pl = inst->plan;
-    cudaError_t e = cudaFuncSetAttribute(lb_kernel<MAXM, EXACT, S16>,
+    // the attribute is per kernel variant and shared by every instance: set it
+    // to the device's opt-in maximum, never to this plan's size
+    cudaError_t e = cudaFuncSetAttribute(lb_kernel<MAXM, EXACT, S16, NPL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)pl.smem_bytes);
+                                         pl.smem_optin);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "cudaFuncSetAttribute");
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM, EXACT, S16>,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM, EXACT, S16, NPL>,
                                                       pl.warps * 32, pl.smem_bytes);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "occupancy");
     if (per_sm < 1) return fsp_fail(FSP_ERANGE, "lb kernel does not fit on an SM");
@@ -445,16 +488,20 @@ int configure(fsp_instance *inst)
     return FSP_OK;
 }
 
-// (MAXM, EXACT, S16) specialisations: exact for Taillard's 5/10/20 machines.
+// (MAXM, EXACT, S16, NPL) specialisations: exact m for Taillard's 5/10/20
+// machines (with 2 or 4 nodes per lane), generic m with 2 nodes per lane.
 #define FSP_DISPATCH_M(FN, S, ...)                                              \
     switch (pl.maxm * 2 + (pl.exact ? 1 : 0)) {                                 \
-    case 5 * 2 + 1: return FN<5, true, S>(__VA_ARGS__);                         \
-    case 10 * 2 + 1: return FN<10, true, S>(__VA_ARGS__);                       \
-    case 20 * 2 + 1: return FN<20, true, S>(__VA_ARGS__);                       \
-    case 8 * 2: return FN<8, false, S>(__VA_ARGS__);                            \
-    case 16 * 2: return FN<16, false, S>(__VA_ARGS__);                          \
-    case 24 * 2: return FN<24, false, S>(__VA_ARGS__);                          \
-    default: return FN<32, false, S>(__VA_ARGS__);                              \
+    case 5 * 2 + 1:                                                             \
+        return pl.npl == 4 ? FN<5, true, S, 4>(__VA_ARGS__) : FN<5, true, S, 2>(__VA_ARGS__); \
+    case 10 * 2 + 1:                                                            \
+        return pl.npl == 4 ? FN<10, true, S, 4>(__VA_ARGS__) : FN<10, true, S, 2>(__VA_ARGS__); \
+    case 20 * 2 + 1:                                                            \
+        return pl.npl == 4 ? FN<20, true, S, 4>(__VA_ARGS__) : FN<20, true, S, 2>(__VA_ARGS__); \
+    case 8 * 2: return FN<8, false, S, 2>(__VA_ARGS__);                         \
+    case 16 * 2: return FN<16, false, S, 2>(__VA_ARGS__);                       \
+    case 24 * 2: return FN<24, false, S, 2>(__VA_ARGS__);                       \
+    default: return FN<32, false, S, 2>(__VA_ARGS__);                           \
     }
 #define FSP_DISPATCH(FN, ...)                                                   \
     if (pl.s16) {                                                               \
@@ -466,6 +513,14 @@ int configure(fsp_instance *inst)
 } // namespace
 
 static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Set the kernel variant's dynamic-smem attribute and fill ctas_per_sm / grid.
+static int occupancy_of(fsp_instance *inst)
+{
+    const fsp_lb_plan &pl = inst->plan;
+    FSP_DISPATCH(configure, inst);
+    return FSP_OK;
+}
 
 static int probe_smem_base(uint32_t *base)
 {
@@ -508,58 +563,71 @@ int fsp_plan_lb(fsp_instance *inst)
     int rc = probe_smem_base(&pl.smem_base);
     if (rc != FSP_OK) return rc;
     pl.num_sms = sms;
+    pl.smem_optin = optin;
     const int mp4 = (m + 3) & ~3;
     pl.nrec = (n + 3) & ~3; // walk steps of 4 positions
-    int want_warps = pl.s16 ? 16 : 8;
-    if (const char *s = getenv("FSP_LB_WARPS")) want_warps = atoi(s);
-    if (want_warps < 1) want_warps = 1;
-    if (want_warps > 16) want_warps = 16;
-    if (pl.maxm > 20 && want_warps > 8) want_warps = 8; // launch bounds of the wide variants
-    // Score each feasible (W, G): more resident warps hide the walk's latency,
-    // each extra couple group costs one table reload per chunk (~1%).
+    pl.npl = 2;
+    // Candidates: nodes per lane (4 only for the exact-m specialisations), warps
+    // per CTA, fewest couple groups that fit.  Score = resident warps per SM
+    // (latency hiding) x 1.3 for 4 nodes per lane (half the table and mask
+    // traffic per node; +10 % measured at 200x20) / (1 + 1.5 % per extra group
+    // reload).  Env FSP_LB_NPL / FSP_LB_WARPS pin a choice (sweeps, tests).
+    int npl_lo = 2, npl_hi = pl.exact ? 4 : 2;
+    if (const char *s = getenv("FSP_LB_NPL")) npl_lo = npl_hi = (atoi(s) == 4 && pl.exact) ? 4 : 2;
+    int w_lo = 1, w_hi = pl.maxm > 20 ? 8 : 16; // launch bounds of the wide variants
+    if (const char *s = getenv("FSP_LB_WARPS")) w_lo = w_hi = std::max(1, std::min(w_hi, atoi(s)));
     double best = -1.0;
-    fsp_lb_layout bestL{};
-    int bestW = 0, bestG = 0, bestPPG = 0;
-    for (int W = want_warps; W >= 1; --W) {
-        fsp_lb_layout L{};
-        L.u_bytes = align16((size_t)(n + 1) * 8 * W);
-        if (pl.smem_base + (size_t)(n + 1) * 8 * W > 65536) continue; // 16-bit U addresses
-        L.off_u = 0;
-        L.ptm_bytes = align16((size_t)n * mp4 * 4);
-        L.off_ptm = L.u_bytes;
-        L.off_bar = L.off_ptm + L.ptm_bytes;
-        L.rt_bytes = 2 * (size_t)pl.maxm * 64 * (pl.s16 ? 2 : 4);
-        L.off_rt = L.off_bar + 16;
-        L.off_tab = align16(L.off_rt + (size_t)W * L.rt_bytes);
-        for (int G = 1; G <= P; ++G) {
-            const int ppg = (P + G - 1) / G;
-            const int Greal = (P + ppg - 1) / ppg;
-            L.kl_bytes = align16((size_t)ppg * 4);
-            // + FSP_REC_SLACK padding records for the walk's look-ahead
-            const size_t gb =
-                align16(L.kl_bytes + ((size_t)ppg * pl.nrec + FSP_REC_SLACK) * sizeof(fsp_rec));
-            if (L.off_tab + gb <= (size_t)optin) {
-                const double score = (double)W / (1.0 + 0.015 * (Greal - 1));
-                if (score > best) {
-                    best = score;
+    fsp_lb_plan bestp = pl;
+    for (int npl = npl_lo; npl <= npl_hi; npl += 2) {
+        for (int W = w_hi; W >= w_lo; --W) {
+            // int32 walk ORs the warp offset into the record address: 4*npl*W
+            // must be a power of two (s16 adds it on the FMA pipe instead)
+            if (!pl.s16 && ((4 * npl * W) & (4 * npl * W - 1))) continue;
+            if (pl.smem_base + (size_t)(n + 1) * 4 * npl * W > 65536) continue; // 16-bit U addresses
+            fsp_lb_layout L{};
+            L.u_bytes = align16((size_t)(n + 1) * 4 * npl * W);
+            L.off_u = 0;
+            L.ptm_bytes = align16((size_t)n * mp4 * 4);
+            L.off_ptm = L.u_bytes;
+            L.off_bar = L.off_ptm + L.ptm_bytes;
+            L.rt_bytes = 2 * (size_t)pl.maxm * 32 * npl * (pl.s16 ? 2 : 4);
+            L.off_rt = L.off_bar + 16;
+            L.off_tab = align16(L.off_rt + (size_t)W * L.rt_bytes);
+            for (int G = 1; G <= P; ++G) {
+                const int ppg = (P + G - 1) / G;
+                const int Greal = (P + ppg - 1) / ppg;
+                L.kl_bytes = align16((size_t)ppg * 4);
+                // + FSP_REC_SLACK padding records for the walk's look-ahead
+                const size_t gb = align16(L.kl_bytes +
+                                          ((size_t)ppg * pl.nrec + FSP_REC_SLACK) * sizeof(fsp_rec));
+                if (L.off_tab + gb <= (size_t)optin) {
+                    fsp_lb_plan c = pl;
                     L.group_bytes = gb;
-                    bestL = L;
-                    bestW = W;
-                    bestG = Greal;
-                    bestPPG = ppg;
+                    c.L = L;
+                    c.npl = npl;
+                    c.groups = Greal;
+                    c.pairs_per_group = ppg;
+                    c.warps = W;
+                    c.smem_bytes = L.off_tab + gb;
+                    fsp_instance tmp = *inst;
+                    tmp.plan = c;
+                    if (occupancy_of(&tmp) == FSP_OK && tmp.plan.ctas_per_sm > 0) {
+                        const double score = (double)W * tmp.plan.ctas_per_sm *
+                                             (npl == 4 ? 1.3 : 1.0) / (1.0 + 0.015 * (Greal - 1));
+                        if (score > best) {
+                            best = score;
+                            bestp = tmp.plan;
+                        }
+                    }
+                    break; // more groups only cost for this (npl, W)
                 }
-                break; // more groups only cost for this W
+                if (ppg == 1) break;
             }
-            if (ppg == 1) break;
         }
     }
     if (best > 0) {
-        pl.L = bestL;
-        pl.groups = bestG;
-        pl.pairs_per_group = bestPPG;
-        pl.warps = bestW;
-        pl.smem_bytes = bestL.off_tab + bestL.group_bytes;
-        FSP_DISPATCH(configure, inst);
+        pl = bestp;
+        return occupancy_of(inst); // sets the attribute for the chosen variant
     }
     return fsp_fail(FSP_ERANGE, "instance tables do not fit in shared memory");
 }

@@ -12,6 +12,8 @@ from paper_1208_3933_b200 import binding, inputs
 
 
 def time_cfg(name, N, warps=None, reps=5):
+    if os.environ.get("FSP_LB_NPL") == "0":
+        os.environ.pop("FSP_LB_NPL")
     if warps:
         os.environ["FSP_LB_WARPS"] = str(warps)
     else:
@@ -43,5 +45,9 @@ if __name__ == "__main__":
     cfgs = sys.argv[1:] or ["ta091"]
     for c in cfgs:
         name, N = (c.split(":") + ["1048576"])[:2]
-        for w in ([int(x) for x in os.environ.get("SWEEP_WARPS", "16,8").split(",")]):
-            print(json.dumps(time_cfg(name, int(N), w)), flush=True)
+        for npl in os.environ.get("SWEEP_NPL", "2,4").split(","):
+            os.environ["FSP_LB_NPL"] = npl
+            for w in ([int(x) for x in os.environ.get("SWEEP_WARPS", "16,8").split(",")]):
+                r = time_cfg(name, int(N), w)
+                r["npl_env"] = int(npl)
+                print(json.dumps(r), flush=True)
