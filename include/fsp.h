@@ -94,6 +94,21 @@ int fsp_instance_get_info(const fsp_instance *inst, fsp_instance_info *info);
 int fsp_lb_eval(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                 const int32_t *depth, int64_t pool, int32_t *lb_out, void *cuda_stream);
 
+/* fsp_lb_eval_sibling — same result as fsp_lb_eval, with the sparse-walk plan
+ * made for B&B child pools: when the nodes of a 64-128 node
+ * block of consecutive entries share most of their unscheduled set (children
+ * of nearby parents), the couple walks visit only the positions of jobs that
+ * are unscheduled in at least one node of the block.
+ *   completion  DEVICE int32 [pool][n_machines] or NULL: each node's prefix
+ *               completion times C_k, e.g. obtained from its
+ *               parent's by one step; when given, the kernel does not
+ *               recompute them from the prefix (the caller guarantees they
+ *               match it: a wrong C gives a wrong LB, never a fault).
+ * Other arguments, layout and errors as fsp_lb_eval. */
+int fsp_lb_eval_sibling(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
+                        const int32_t *depth, const int32_t *completion, int64_t pool,
+                        int32_t *lb_out, void *cuda_stream);
+
 /* fsp_lb_eval_host — same result with HOST buffers (the paper's offload
  * round trip): copies the pool to the device in chunks, bounds each
  * chunk and copies the LBs back, overlapping the three on two streams.

@@ -53,6 +53,16 @@ extern "C" int fsp_lb_eval(const fsp_instance *inst, const uint16_t *prefix, int
                          static_cast<cudaStream_t>(cuda_stream));
 }
 
+extern "C" int fsp_lb_eval_sibling(const fsp_instance *inst, const uint16_t *prefix,
+                                   int32_t stride, const int32_t *depth, const int32_t *completion,
+                                   int64_t pool, int32_t *lb_out, void *cuda_stream)
+{
+    int rc = check_args(inst, prefix, stride, depth, pool, lb_out);
+    if (rc != FSP_OK || pool == 0) return rc;
+    return fsp_launch_lb_dev(inst, prefix, stride, depth, pool, nullptr, completion, inst->m, true,
+                             lb_out, static_cast<cudaStream_t>(cuda_stream));
+}
+
 extern "C" int fsp_check(const fsp_instance *inst, void *cuda_stream)
 {
     if (!inst) return fsp_fail(FSP_EINVAL, "null instance");

@@ -2,18 +2,23 @@
 //
 // The four operators of §II-A with the paper's forward branching
 // and elimination LB >= incumbent (R9), all on the device:
-//   selection  (a9)  the top B open nodes of a device stack: deepest-first
-//                    batches replace the paper's host best-first list (R10);
-//   branching  (a7)  expand_kernel writes every child prefix + j, j unscheduled,
-//                    ascending j;
-//   bounding   (a1-a5) the LB kernel of lb_kernel.cu on the child pool, pool
-//                    size read on the device;
-//   elimination (a6) prune_kernel + scan + scatter_kernel: survivors LB <
-//                    incumbent are stream-compacted back onto the stack in
-//                    child order; leaves (depth >= n-1, whose LB is their exact
-//                    makespan, R6) feed a packed (makespan, index) atomicMin and
-//                    commit_kernel adopts the best one with its permutation (a8).
-// One 24-byte status read per iteration is the only host round trip.
+//   selection  (a9)  the top B open nodes of a device stack (deepest-first
+//                    batches replace the paper's host best-first list, R10);
+//   branching  (a7)  lazy: a popped parent generates its next K children
+//                    (prefix + j, j unscheduled, ascending j) and, if
+//                    it has more, goes back on the stack below them with an
+//                    advanced cursor (bounded memory); each
+//                    child's completion times come from its parent's in one step;
+//   bounding   (a1-a5) the LB kernel on the child pool with the sparse-walk plan
+//                    (children of nearby parents share most of their
+//                    unscheduled set), pool size read on the device;
+//   elimination (a6) prune + scan + scatter: survivors (LB < incumbent) are
+//                    stream-compacted onto the stack in child order, parents
+//                    whose stored LB reached the incumbent are dropped at pop;
+//                    leaves (depth >= n-1: LB is the exact makespan, R6/P4) feed
+//                    a packed (makespan, index) atomicMin and commit_kernel
+//                    adopts the best one with its permutation (a8).
+// One small status read per iteration is the only host round trip.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,102 +39,136 @@ constexpr unsigned long long kNoCand = ~0ull;
 
 struct BBStatus {
     long long children;  // children bounded this iteration
-    long long survivors; // pushed back onto the stack
+    long long kept;      // popped parents pushed back (more children to come)
+    long long survivors; // children pushed onto the stack
     int incumbent;       // current incumbent (INT_MAX = none)
-    int improved;        // incumbent improved this iteration
+    int improved;        // this rank's incumbent improved this iteration
+};
+
+// Open nodes, structure of arrays: prefix, depth, completion times C[m],
+// cursor (children already generated), LB from when the node was bounded.
+struct Nodes {
+    uint16_t *pf = nullptr;
+    int32_t *dp = nullptr, *C = nullptr, *cur = nullptr, *lb = nullptr;
 };
 
 struct BBState {
     const fsp_instance *inst;
-    int rank, world, n, stride;
-    int64_t cap;         // stack capacity (nodes)
-    int64_t base, size;  // open nodes live in [base, size)
-    int64_t ccap;        // child buffer capacity
-    uint16_t *st_pf;     // stack prefixes [cap][stride]
-    int32_t *st_dp;      // stack depths
-    uint16_t *ch_pf;     // children [ccap][stride]
-    int32_t *ch_dp, *ch_lb;
-    int64_t *off;        // children offsets per parent [ccap/1 + 1]
-    int64_t *boff;       // survivor offsets per prune block
-    int32_t *bcnt;       // survivor count per prune block
-    int32_t *d_inc;      // incumbent makespan
+    int rank, world, n, m, stride, K;
+    int64_t cap;          // stack capacity (nodes)
+    int64_t base, size;   // open nodes live in [base, size)
+    int64_t ccap;         // children per iteration (buffer capacity)
+    int64_t kcap;         // parents per iteration
+    Nodes st, kp, ch;     // stack, kept parents (scratch), children
+    long long *plan;      // per parent: (keep << 32) | children now
+    int64_t *off;         // exclusive scan of plan; off[B] = (kept << 32) | children
+    int64_t *d_count;     // children this iteration (LB pool size)
+    int64_t *boff;        // survivor offsets per prune block
+    int32_t *bcnt;
+    int32_t *d_inc;       // incumbent makespan (pruning threshold)
     unsigned long long *d_cand;
-    long long *d_packed; // (incumbent << 32) | rank for the MIN all-reduce
+    long long *d_packed;  // (own best << 32) | rank for the MIN all-reduce
     long long *d_scratch;
-    int32_t *d_perm;     // incumbent permutation
+    int32_t *d_perm;      // this rank's best permutation
     unsigned long long *d_stats; // [pruned, leaves]
-    BBStatus *d_status;
-    BBStatus *h_status;  // pinned
+    BBStatus *d_status, *h_status;
     cudaStream_t stream;
-    bool own_stream;
+    bool own_stream, sparse;
     fsp_bb_stats stats;
-    int have;            // this rank holds a permutation ...
-    int32_t perm_ms;     // ... of this makespan (the incumbent may be lower: adopted)
-    double kids_per_parent; // running estimate for the batch size
-    int32_t initial_inc; // initial_ub + 1 (saturating)
+    int have;             // this rank holds a permutation ...
+    int32_t perm_ms;      // ... of this makespan (the incumbent may be lower: adopted)
+    int32_t initial_inc;  // initial_ub + 1 (saturating)
 };
 
-__device__ __forceinline__ int warp_excl_scan(int v, int lane, int &total)
+__device__ __forceinline__ long long warp_excl_scan64(long long v, int lane, long long &total)
 {
-    int x = v;
+    long long x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, x, o);
+        const long long y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
     total = __shfl_sync(0xffffffffu, x, 31);
     return x - v;
 }
 
-// Block-wide exclusive scan of one int per thread (blockDim multiple of 32).
-__device__ __forceinline__ long long block_excl_scan(int v, long long &total)
+// Block-wide exclusive scan of one int64 per thread (blockDim multiple of 32).
+__device__ __forceinline__ long long block_excl_scan(long long v, long long &total)
 {
-    __shared__ int wsum[32];
+    __shared__ long long wsum[32];
     __shared__ long long s_tot;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    int wt;
-    const int ex = warp_excl_scan(v, lane, wt);
+    long long wt;
+    const long long ex = warp_excl_scan64(v, lane, wt);
     if (lane == 31) wsum[warp] = wt;
     __syncthreads();
     if (warp == 0) {
-        const int x = lane < nw ? wsum[lane] : 0;
-        int t;
-        const int e = warp_excl_scan(x, lane, t);
+        const long long x = lane < nw ? wsum[lane] : 0;
+        long long t;
+        const long long e = warp_excl_scan64(x, lane, t);
         if (lane < nw) wsum[lane] = e;
         if (lane == 0) s_tot = t;
     }
     __syncthreads();
-    const long long r = (long long)ex + wsum[warp];
+    const long long r = ex + wsum[warp];
     total = s_tot;
     __syncthreads(); // wsum / s_tot are reused by the next call
     return r;
 }
 
-// Exclusive scan over N items, single block.  mode 0: item i = n - depth[i]
-// (children of parent i); mode 1: item i = cnt[i].  out[N] = total.
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(int mode, const int32_t *depth, int n,
-                                                            const int32_t *cnt, const int64_t *N_dev,
-                                                            int64_t N_host, int64_t *out)
+// Exclusive scan of N items (single block); out[N] = total.  Items are int64
+// (in64) or int32 (in32).  If count_out: *count_out = low 32 bits of the total.
+__global__ void __launch_bounds__(kScanThreads)
+    scan_kernel(const long long *in64, const int32_t *in32, int64_t N, int64_t *out,
+                int64_t *count_out)
 {
-    const int64_t N = N_dev ? *N_dev : N_host;
     long long carry = 0;
     for (int64_t t0 = 0; t0 < N; t0 += blockDim.x) {
         const int64_t i = t0 + threadIdx.x;
-        int v = 0;
-        if (i < N) v = mode == 0 ? n - depth[i] : cnt[i];
+        long long v = 0;
+        if (i < N) v = in64 ? in64[i] : (long long)in32[i];
         long long tot;
         const long long ex = block_excl_scan(v, tot);
         if (i < N) out[i] = carry + ex;
         carry += tot;
     }
-    if (threadIdx.x == 0) out[N] = carry;
+    if (threadIdx.x == 0) {
+        out[N] = carry;
+        if (count_out) *count_out = carry & 0xffffffffll;
+    }
 }
 
-// Branching (a7): one warp per parent; children are prefix + j for every
-// unscheduled j in ascending order.
-__global__ void expand_kernel(const uint16_t *__restrict__ st_pf, const int32_t *__restrict__ st_dp,
-                              int64_t first, int64_t B, const int64_t *__restrict__ off,
-                              uint16_t *__restrict__ ch_pf, int32_t *__restrict__ ch_dp, int n,
+// Selection (a9) bookkeeping: per popped parent, children to generate now
+// (at most K) and whether it stays open.  A parent whose LB (bounded when it
+// was a child) has reached the incumbent since is eliminated here (R9).
+__global__ void plan_kernel(Nodes st, int64_t first, int64_t B, int n, int K, const int32_t *inc_dev,
+                            long long *plan, unsigned long long *stats)
+{
+    const int inc = *inc_dev;
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int dropped = 0;
+    if (p < B) {
+        const int64_t i = first + p;
+        long long g = 0, keep = 0;
+        if (st.lb[i] < inc) {
+            const int r = n - st.dp[i] - st.cur[i];
+            g = r < K ? r : K;
+            keep = r > g;
+        } else {
+            dropped = 1;
+        }
+        plan[p] = (keep << 32) | g;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, dropped);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(&stats[0], (unsigned long long)__popc(b));
+}
+
+// Branching (a7): one warp per parent; its unscheduled jobs of ascending rank
+// cur .. cur+g-1 become children prefix + j with C'_0 = C_0 + p_j0,
+// C'_k = max(C'_k-1, C_k) + p_jk; a parent with children left is
+// copied to the kept buffer with its cursor advanced.
+__global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t *__restrict__ off,
+                              Nodes ch, Nodes kp, const int32_t *__restrict__ ptm, int n, int m,
                               int stride)
 {
     extern __shared__ uint32_t bm_all[];
@@ -138,44 +177,91 @@ __global__ void expand_kernel(const uint16_t *__restrict__ st_pf, const int32_t 
     uint32_t *bm = bm_all + wib * nw;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; p < B; p += warps) {
-        const uint16_t *row = st_pf + (size_t)(first + p) * stride;
-        const int d = st_dp[first + p];
-        for (int w = lane; w < nw; w += 32) bm[w] = 0;
-        __syncwarp();
-        for (int i = lane; i < d; i += 32) atomicOr(&bm[row[i] >> 5], 1u << (row[i] & 31));
-        __syncwarp();
-        int64_t c = off[p];
-        for (int w = 0; w < nw; ++w) {
-            uint32_t freeb = ~bm[w];
-            if (w == nw - 1 && (n & 31)) freeb &= (1u << (n & 31)) - 1;
-            while (freeb) {
-                const int j = w * 32 + __ffs(freeb) - 1;
-                freeb &= freeb - 1;
-                uint16_t *crow = ch_pf + (size_t)c * stride;
-                for (int i = lane; i < d; i += 32) crow[i] = row[i];
-                if (lane == 0) {
-                    crow[d] = (uint16_t)j;
-                    ch_dp[c] = d + 1;
+        const int64_t src = first + p;
+        const uint16_t *row = st.pf + (size_t)src * stride;
+        const int d = st.dp[src], cur = st.cur[src];
+        const long long o0 = off[p], o1 = off[p + 1];
+        const int g = (int)((o1 & 0xffffffffll) - (o0 & 0xffffffffll));
+        const int keep = (int)((o1 >> 32) - (o0 >> 32));
+        int64_t c = o0 & 0xffffffffll;
+        if (g > 0) {
+            for (int w = lane; w < nw; w += 32) bm[w] = 0;
+            __syncwarp();
+            for (int i = lane; i < d; i += 32) atomicOr(&bm[row[i] >> 5], 1u << (row[i] & 31));
+            __syncwarp();
+            int rank = 0;
+            for (int w = 0; w < nw && rank < cur + g; ++w) {
+                uint32_t freeb = ~bm[w];
+                if (w == nw - 1 && (n & 31)) freeb &= (1u << (n & 31)) - 1;
+                while (freeb && rank < cur + g) {
+                    const int j = w * 32 + __ffs(freeb) - 1;
+                    freeb &= freeb - 1;
+                    if (rank++ < cur) continue;
+                    uint16_t *crow = ch.pf + (size_t)c * stride;
+                    for (int i = lane; i < d; i += 32) crow[i] = row[i];
+                    if (lane == 0) {
+                        crow[d] = (uint16_t)j;
+                        ch.dp[c] = d + 1;
+                        const int32_t *pc = st.C + (size_t)src * m;
+                        int32_t *cc = ch.C + (size_t)c * m;
+                        int prev = 0;
+                        for (int k = 0; k < m; ++k) {
+                            prev = max(prev, pc[k]) + ptm[j * m + k];
+                            cc[k] = prev;
+                        }
+                    }
+                    ++c;
                 }
-                ++c;
+            }
+        }
+        if (keep) {
+            const int64_t dst = o0 >> 32;
+            uint16_t *krow = kp.pf + (size_t)dst * stride;
+            for (int i = lane; i < d; i += 32) krow[i] = row[i];
+            for (int k = lane; k < m; k += 32) kp.C[(size_t)dst * m + k] = st.C[(size_t)src * m + k];
+            if (lane == 0) {
+                kp.dp[dst] = d;
+                kp.cur[dst] = cur + g;
+                kp.lb[dst] = st.lb[src];
             }
         }
         __syncwarp();
     }
 }
 
+// Kept parents back onto the stack at [first, first + kept).
+__global__ void restore_kernel(Nodes kp, const int64_t *off_B, int64_t first, Nodes st, int m,
+                               int stride)
+{
+    const int64_t Pk = *off_B >> 32;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < Pk;
+         q += warps) {
+        const int d = kp.dp[q];
+        const int64_t dst = first + q;
+        for (int i = lane; i < d; i += 32)
+            st.pf[(size_t)dst * stride + i] = kp.pf[(size_t)q * stride + i];
+        for (int k = lane; k < m; k += 32) st.C[(size_t)dst * m + k] = kp.C[(size_t)q * m + k];
+        if (lane == 0) {
+            st.dp[dst] = d;
+            st.cur[dst] = kp.cur[q];
+            st.lb[dst] = kp.lb[q];
+        }
+    }
+}
+
 // Elimination (a6) + leaves (a8): count survivors per block.
 __global__ void __launch_bounds__(kPruneThreads)
-    prune_kernel(const int32_t *__restrict__ ch_dp, const int32_t *__restrict__ ch_lb,
-                 const int64_t *C_dev, int n, const int32_t *inc_dev, unsigned long long *cand,
-                 int32_t *bcnt, unsigned long long *stats)
+    prune_kernel(Nodes ch, const int64_t *count, int n, const int32_t *inc_dev,
+                 unsigned long long *cand, int32_t *bcnt, unsigned long long *stats)
 {
-    const int64_t C = *C_dev;
+    const int64_t C = *count;
     const int inc = *inc_dev;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int survive = 0, pruned = 0, leaf = 0;
     if (i < C) {
-        const int d = ch_dp[i], lb = ch_lb[i];
+        const int d = ch.dp[i], lb = ch.lb[i];
         if (d >= n - 1) { // complete or forced completion: LB is its makespan (R6, P4)
             leaf = 1;
             if (lb < inc) atomicMin(cand, ((unsigned long long)(unsigned)lb << 32) | (unsigned)i);
@@ -195,45 +281,44 @@ __global__ void __launch_bounds__(kPruneThreads)
     }
 }
 
-// Stream compaction of the survivors onto the stack at `top`, child order.
+// Stream compaction of the survivors onto the stack above the kept parents.
 __global__ void __launch_bounds__(kPruneThreads)
-    scatter_kernel(const uint16_t *__restrict__ ch_pf, const int32_t *__restrict__ ch_dp,
-                   const int32_t *__restrict__ ch_lb, const int64_t *C_dev, int n, int stride,
-                   const int32_t *inc_dev, const int64_t *__restrict__ boff, int64_t top,
-                   uint16_t *__restrict__ st_pf, int32_t *__restrict__ st_dp)
+    scatter_kernel(Nodes ch, const int64_t *count, const int64_t *off_B, int n, int m, int stride,
+                   const int32_t *inc_dev, const int64_t *__restrict__ boff, int64_t first, Nodes st)
 {
     __shared__ int64_t s_dst[kPruneThreads];
     __shared__ int64_t s_src[kPruneThreads];
-    const int64_t C = *C_dev;
+    const int64_t C = *count;
+    const int64_t top = first + (*off_B >> 32);
     const int inc = *inc_dev;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int survive = 0, d = 0;
-    if (i < C) {
-        d = ch_dp[i];
-        survive = d < n - 1 && ch_lb[i] < inc;
-    }
+    int survive = 0;
+    if (i < C) survive = ch.dp[i] < n - 1 && ch.lb[i] < inc;
     long long tot;
     const long long r = block_excl_scan(survive, tot);
     if (survive) {
-        s_dst[r] = top + boff[blockIdx.x] + r;
+        const int64_t dst = top + boff[blockIdx.x] + r;
+        s_dst[r] = dst;
         s_src[r] = i;
-        st_dp[top + boff[blockIdx.x] + r] = d;
+        st.dp[dst] = ch.dp[i];
+        st.cur[dst] = 0;
+        st.lb[dst] = ch.lb[i];
     }
     __syncthreads();
     // warp-cooperative, coalesced row copies
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
     for (int k = wib; k < tot; k += nwb) {
-        const uint16_t *src = ch_pf + (size_t)s_src[k] * stride;
-        uint16_t *dst = st_pf + (size_t)s_dst[k] * stride;
-        const int dd = ch_dp[s_src[k]];
-        for (int q = lane; q < dd; q += 32) dst[q] = src[q];
+        const int64_t src = s_src[k], dst = s_dst[k];
+        const int dd = ch.dp[src];
+        for (int q = lane; q < dd; q += 32)
+            st.pf[(size_t)dst * stride + q] = ch.pf[(size_t)src * stride + q];
+        for (int q = lane; q < m; q += 32) st.C[(size_t)dst * m + q] = ch.C[(size_t)src * m + q];
     }
 }
 
 // Adopt the best leaf of this iteration (a8) and publish the status.
-__global__ void commit_kernel(const uint16_t *__restrict__ ch_pf, const int32_t *__restrict__ ch_dp,
-                              int n, int stride, int32_t *inc, unsigned long long *cand,
-                              int32_t *perm, long long *packed, int rank, const int64_t *C_dev,
+__global__ void commit_kernel(Nodes ch, int n, int stride, int32_t *inc, unsigned long long *cand,
+                              int32_t *perm, long long *packed, int rank, const int64_t *off_B,
                               const int64_t *T_dev, BBStatus *status)
 {
     __shared__ int s_improved;
@@ -245,8 +330,8 @@ __global__ void commit_kernel(const uint16_t *__restrict__ ch_pf, const int32_t 
         const int mk = (int)(c >> 32);
         const int64_t idx = (int64_t)(c & 0xffffffffull);
         if (mk < *inc) {
-            const uint16_t *row = ch_pf + (size_t)idx * stride;
-            const int d = ch_dp[idx];
+            const uint16_t *row = ch.pf + (size_t)idx * stride;
+            const int d = ch.dp[idx];
             for (int w = threadIdx.x; w < (n + 31) / 32; w += blockDim.x) s_bm[w] = 0;
             __syncthreads();
             for (int i = threadIdx.x; i < d; i += blockDim.x) {
@@ -269,8 +354,9 @@ __global__ void commit_kernel(const uint16_t *__restrict__ ch_pf, const int32_t 
         // (own best << 32) | rank: the MIN over ranks names the holder of the
         // best permutation (an adopted incumbent only tightens pruning)
         if (s_improved) *packed = ((long long)*inc << 32) | (unsigned)rank;
-        status->children = C_dev ? *C_dev : 0;
-        status->survivors = T_dev ? *T_dev : 0;
+        status->children = *off_B & 0xffffffffll;
+        status->kept = *off_B >> 32;
+        status->survivors = *T_dev;
         status->incumbent = *inc;
         status->improved = s_improved;
     }
@@ -284,15 +370,25 @@ __global__ void adopt_ub_kernel(int32_t *inc, const long long *src)
 
 int cuda_or(cudaError_t e, const char *what) { return e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, what); }
 
+void free_nodes(Nodes &x)
+{
+    cudaFree(x.pf);
+    cudaFree(x.dp);
+    cudaFree(x.C);
+    cudaFree(x.cur);
+    cudaFree(x.lb);
+    x = Nodes();
+}
+
 void bb_free(BBState *s)
 {
     if (!s) return;
-    cudaFree(s->st_pf);
-    cudaFree(s->st_dp);
-    cudaFree(s->ch_pf);
-    cudaFree(s->ch_dp);
-    cudaFree(s->ch_lb);
+    free_nodes(s->st);
+    free_nodes(s->kp);
+    free_nodes(s->ch);
+    cudaFree(s->plan);
     cudaFree(s->off);
+    cudaFree(s->d_count);
     cudaFree(s->boff);
     cudaFree(s->bcnt);
     cudaFree(s->d_inc);
@@ -313,84 +409,140 @@ int64_t env_i64(const char *name, int64_t dflt)
     return v ? atoll(v) : dflt;
 }
 
-// Push nodes given as (depth, prefix) host rows onto the stack top.
+size_t node_bytes(const BBState *s) { return (size_t)s->stride * 2 + 12 + (size_t)s->m * 4; }
+
+cudaError_t alloc_nodes(Nodes &x, int64_t cnt, int stride, int m)
+{
+    cudaError_t e = cudaMalloc(&x.pf, (size_t)cnt * stride * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&x.dp, (size_t)cnt * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&x.C, (size_t)cnt * m * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&x.cur, (size_t)cnt * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&x.lb, (size_t)cnt * 4);
+    return e;
+}
+
+// Copy k nodes between node arrays (device to device, stream-ordered).
+cudaError_t copy_nodes(const BBState *s, Nodes dst, int64_t di, Nodes src, int64_t si, int64_t k)
+{
+    const int st = s->stride, m = s->m;
+    cudaStream_t q = s->stream;
+    cudaError_t e = cudaMemcpyAsync(dst.pf + (size_t)di * st, src.pf + (size_t)si * st,
+                                    (size_t)k * st * 2, cudaMemcpyDeviceToDevice, q);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dst.dp + di, src.dp + si, (size_t)k * 4, cudaMemcpyDeviceToDevice, q);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dst.C + (size_t)di * m, src.C + (size_t)si * m, (size_t)k * m * 4,
+                            cudaMemcpyDeviceToDevice, q);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dst.cur + di, src.cur + si, (size_t)k * 4, cudaMemcpyDeviceToDevice, q);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dst.lb + di, src.lb + si, (size_t)k * 4, cudaMemcpyDeviceToDevice, q);
+    return e;
+}
+
+// A flat buffer of k nodes viewed as node arrays:
+// [k][stride] u16 prefixes | [k] depth | [k][m] C | [k] cursor | [k] LB.
+Nodes flat_view(const BBState *s, const void *buf, int64_t k)
+{
+    uint8_t *b = static_cast<uint8_t *>(const_cast<void *>(buf));
+    Nodes x;
+    x.pf = reinterpret_cast<uint16_t *>(b);
+    b += (size_t)k * s->stride * 2;
+    x.dp = reinterpret_cast<int32_t *>(b);
+    b += (size_t)k * 4;
+    x.C = reinterpret_cast<int32_t *>(b);
+    b += (size_t)k * s->m * 4;
+    x.cur = reinterpret_cast<int32_t *>(b);
+    b += (size_t)k * 4;
+    x.lb = reinterpret_cast<int32_t *>(b);
+    return x;
+}
+
+// Push nodes given as (depth, prefix) host rows onto the stack top; their
+// completion times are computed here from the prefixes.
 int push_host(BBState *s, const std::vector<uint16_t> &pf, const std::vector<int32_t> &dp)
 {
     const int64_t k = (int64_t)dp.size();
     if (s->size + k > s->cap) return fsp_fail(FSP_ENOMEM, "B&B stack full");
-    cudaError_t e = cudaMemcpyAsync(s->st_pf + (size_t)s->size * s->stride, pf.data(),
-                                    sizeof(uint16_t) * pf.size(), cudaMemcpyHostToDevice, s->stream);
+    const int m = s->m;
+    const int32_t *ptm = s->inst->h_ptm;
+    std::vector<int32_t> C((size_t)k * m, 0), zero((size_t)k, 0);
+    for (int64_t i = 0; i < k; ++i) {
+        int32_t *c = &C[(size_t)i * m];
+        for (int q = 0; q < dp[i]; ++q) {
+            const int j = pf[(size_t)i * s->stride + q];
+            int prev = 0;
+            for (int t = 0; t < m; ++t) {
+                prev = std::max(prev, c[t]) + ptm[(size_t)j * m + t];
+                c[t] = prev;
+            }
+        }
+    }
+    const int64_t at = s->size;
+    cudaStream_t q = s->stream;
+    cudaError_t e = cudaMemcpyAsync(s->st.pf + (size_t)at * s->stride, pf.data(),
+                                    sizeof(uint16_t) * pf.size(), cudaMemcpyHostToDevice, q);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(s->st_dp + s->size, dp.data(), sizeof(int32_t) * k,
-                            cudaMemcpyHostToDevice, s->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+        e = cudaMemcpyAsync(s->st.dp + at, dp.data(), 4 * k, cudaMemcpyHostToDevice, q);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(s->st.C + (size_t)at * m, C.data(), 4 * C.size(), cudaMemcpyHostToDevice, q);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(s->st.cur + at, zero.data(), 4 * k, cudaMemcpyHostToDevice, q);
+    if (e == cudaSuccess) // never bounded: LB 0, never eliminated at pop
+        e = cudaMemcpyAsync(s->st.lb + at, zero.data(), 4 * k, cudaMemcpyHostToDevice, q);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(q);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "B&B push");
     s->size += k;
     return FSP_OK;
 }
 
-// One expand/bound/prune iteration.  Returns FSP_OK (or an error).
+// One select / branch / bound / eliminate iteration.
 int bb_iterate(BBState *s)
 {
     const fsp_instance *inst = s->inst;
-    const int n = s->n, stride = s->stride;
+    const int n = s->n, m = s->m, stride = s->stride, K = s->K;
     cudaStream_t st = s->stream;
     const int64_t open = s->size - s->base;
     if (open <= 0) return FSP_OK;
-    // selection: the top B nodes (deepest-first batch), sized from the last
-    // iteration's children per parent so the child pool fills the GPU; the
-    // exact child count is checked after the scan and B halved if it overflows
-    const double kpp = std::max(1.0, std::min((double)n, s->kids_per_parent));
-    int64_t B = std::min<int64_t>(open, std::max<int64_t>(1, (int64_t)(s->ccap / kpp)));
-    // beam width of the depth-first batches: B parents per level with ~n/2
-    // children each over n levels must fit the stack (B * n^2/2 <= cap)
-    B = std::min<int64_t>(B, std::max<int64_t>(1, s->cap / std::max<int64_t>(1, (int64_t)n * n / 2)));
-    // keep n*n slots of headroom: from any state a depth-first descent (B = 1)
-    // needs at most n children per level for n levels, so the search never
-    // dead-ends on memory
-    const int64_t usable = s->cap - (int64_t)n * n;
-    int64_t first = 0;
-    for (;;) {
-        first = s->size - B;
-        scan_kernel<<<1, kScanThreads, 0, st>>>(0, s->st_dp + first, n, nullptr, nullptr, B, s->off);
-        cudaError_t e = cudaMemcpyAsync(&s->h_status->children, s->off + B, 8,
-                                        cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) return fsp_cuda_fail(e, "B&B scan");
-        const long long C = s->h_status->children;
-        // the children must fit the child buffer, and (all surviving) the stack
-        const int64_t room = std::max<int64_t>(0, std::min<int64_t>(s->ccap, usable - first));
-        if (C <= room) break;
-        if (B == 1) {
-            if (first + C > s->cap || C > s->ccap) return fsp_fail(FSP_ENOMEM, "B&B stack full");
-            break;
-        }
-        B = std::max<int64_t>(1, std::min<int64_t>(B / 2, (int64_t)((double)B * room / (double)C * 0.9)));
-    }
-    s->size = first;
-    const int64_t maxC = s->h_status->children;
+    // B parents: at most K children each fit the child buffer; the stack grows
+    // by at most B*K per iteration and B*K*n over a descent, held under half
+    // the capacity (the beam); n*K slots of headroom are always left
+    const int64_t usable = s->cap - (int64_t)n * K;
+    int64_t B = std::min<int64_t>(open, std::min<int64_t>(s->kcap, s->ccap / K));
+    B = std::min<int64_t>(B, std::max<int64_t>(1, s->cap / 2 / ((int64_t)K * n)));
+    B = std::min<int64_t>(B, std::max<int64_t>(1, (usable - s->size) / K));
+    if (s->size + B * K > s->cap) return fsp_fail(FSP_ENOMEM, "B&B stack full");
+    const int64_t first = s->size - B;
 
+    const int pb = 256;
+    plan_kernel<<<(unsigned)((B + pb - 1) / pb), pb, 0, st>>>(s->st, first, B, n, K, s->d_inc,
+                                                              s->plan, s->d_stats);
+    scan_kernel<<<1, kScanThreads, 0, st>>>(s->plan, nullptr, B, s->off, s->d_count);
     const int ewarps = 8;
     const int eblocks = (int)std::min<int64_t>((B + ewarps - 1) / ewarps, 148 * 16);
     expand_kernel<<<eblocks, ewarps * 32, ewarps * ((n + 31) / 32) * 4, st>>>(
-        s->st_pf, s->st_dp, first, B, s->off, s->ch_pf, s->ch_dp, n, stride);
-    const int64_t *C_dev = s->off + B;
-    int rc = fsp_launch_lb_dev(inst, s->ch_pf, stride, s->ch_dp, maxC, C_dev, s->ch_lb, st);
+        s->st, first, B, s->off, s->ch, s->kp, inst->d_ptm32, n, m, stride);
+    const int64_t *off_B = s->off + B; // (kept << 32) | children, on the device
+    restore_kernel<<<eblocks, ewarps * 32, 0, st>>>(s->kp, off_B, first, s->st, m, stride);
+    // bounding: pool size read on the device, C from the parents, sparse walk
+    const int64_t maxC = B * K;
+    int rc = fsp_launch_lb_dev(inst, s->ch.pf, stride, s->ch.dp, maxC, s->d_count, s->ch.C, m,
+                               s->sparse, s->ch.lb, st);
     if (rc != FSP_OK) return rc;
     const int nblk = (int)((maxC + kPruneThreads - 1) / kPruneThreads);
-    prune_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch_dp, s->ch_lb, C_dev, n, s->d_inc, s->d_cand,
-                                                  s->bcnt, s->d_stats);
-    scan_kernel<<<1, kScanThreads, 0, st>>>(1, nullptr, n, s->bcnt, nullptr, nblk, s->boff);
-    scatter_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch_pf, s->ch_dp, s->ch_lb, C_dev, n, stride,
-                                                    s->d_inc, s->boff, first, s->st_pf, s->st_dp);
-    commit_kernel<<<1, 256, 0, st>>>(s->ch_pf, s->ch_dp, n, stride, s->d_inc, s->d_cand, s->d_perm,
-                                     s->d_packed, s->rank, C_dev, s->boff + nblk, s->d_status);
+    prune_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->d_count, n, s->d_inc, s->d_cand, s->bcnt,
+                                                  s->d_stats);
+    scan_kernel<<<1, kScanThreads, 0, st>>>(nullptr, s->bcnt, nblk, s->boff, nullptr);
+    scatter_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->d_count, off_B, n, m, stride, s->d_inc,
+                                                    s->boff, first, s->st);
+    commit_kernel<<<1, 256, 0, st>>>(s->ch, n, stride, s->d_inc, s->d_cand, s->d_perm, s->d_packed,
+                                     s->rank, off_B, s->boff + nblk, s->d_status);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(s->h_status, s->d_status, sizeof(BBStatus), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "B&B iteration");
-    s->size = first + s->h_status->survivors;
+    s->size = first + s->h_status->kept + s->h_status->survivors;
     s->stats.bounded += s->h_status->children;
     s->stats.branched += B;
     s->stats.iterations += 1;
@@ -398,8 +550,6 @@ int bb_iterate(BBState *s)
         s->have = 1;
         s->perm_ms = s->h_status->incumbent;
     }
-    if (B > 0 && s->h_status->children > 0)
-        s->kids_per_parent = (double)s->h_status->children / (double)B;
     return FSP_OK;
 }
 
@@ -414,8 +564,11 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     s->rank = rank;
     s->world = world;
     s->n = inst->n;
+    s->m = inst->m;
     s->stride = (inst->n + 7) & ~7;
     s->initial_inc = initial_ub == INT32_MAX ? INT32_MAX : initial_ub + 1; // R9
+    s->sparse = getenv("FSP_BB_SPARSE") ? atoi(getenv("FSP_BB_SPARSE")) != 0 : true;
+    s->K = (int)std::max<int64_t>(1, env_i64("FSP_BB_K", 8)); // children per parent per pop
     cudaError_t e = cudaSuccess;
     if (stream) {
         s->stream = static_cast<cudaStream_t>(stream);
@@ -423,30 +576,28 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
         e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
         s->own_stream = true;
     }
-    const int n = s->n;
-    const size_t rec = (size_t)s->stride * 2 + 4;
+    const int n = s->n, m = s->m;
     size_t freeb = 0, totalb = 0;
     if (e == cudaSuccess) e = cudaMemGetInfo(&freeb, &totalb);
-    // child buffer: enough children to fill the GPU several times over
-    s->ccap = env_i64("FSP_BB_CHILDREN", std::max<int64_t>(1 << 22, (int64_t)n * 4));
-    s->kids_per_parent = n;
-    // the stack may take most of the free HBM (180 GB per B200): its size bounds
-    // the beam width of the depth-first batches (see bb_iterate)
-    const double frac = getenv("FSP_BB_MEM_FRAC") ? atof(getenv("FSP_BB_MEM_FRAC")) : 0.6;
-    int64_t cap = (int64_t)((double)freeb * frac / rec);
+    // children per iteration: enough to fill the GPU several times over
+    s->ccap = std::max<int64_t>(env_i64("FSP_BB_CHILDREN", 1 << 21), s->K);
+    s->kcap = s->ccap;
+    // the stack takes most of the free HBM (180 GB per B200)
+    const double frac = getenv("FSP_BB_MEM_FRAC") ? atof(getenv("FSP_BB_MEM_FRAC")) : 0.5;
+    const size_t buffers = (size_t)(s->ccap + s->kcap) * node_bytes(s);
+    int64_t cap = freeb > buffers ? (int64_t)((double)(freeb - buffers) * frac / node_bytes(s)) : 0;
     cap = env_i64("FSP_BB_STACK", std::min<int64_t>(cap, (int64_t)1 << 31));
-    s->cap = std::max<int64_t>(cap, (int64_t)n * n * 4);
-    const int64_t maxB = s->ccap; // parents per iteration never exceed the children
+    s->cap = std::max<int64_t>(cap, (int64_t)n * s->K * 4);
     const int64_t nblk = (s->ccap + kPruneThreads - 1) / kPruneThreads + 1;
+    if (e == cudaSuccess) e = alloc_nodes(s->st, s->cap, s->stride, m);
+    if (e == cudaSuccess) e = alloc_nodes(s->kp, s->kcap, s->stride, m);
+    if (e == cudaSuccess) e = alloc_nodes(s->ch, s->ccap, s->stride, m);
     auto alloc = [&](void **p, size_t bytes) {
         if (e == cudaSuccess) e = cudaMalloc(p, bytes);
     };
-    alloc((void **)&s->st_pf, (size_t)s->cap * s->stride * 2);
-    alloc((void **)&s->st_dp, (size_t)s->cap * 4);
-    alloc((void **)&s->ch_pf, (size_t)s->ccap * s->stride * 2);
-    alloc((void **)&s->ch_dp, (size_t)s->ccap * 4);
-    alloc((void **)&s->ch_lb, (size_t)s->ccap * 4);
-    alloc((void **)&s->off, (size_t)(maxB + 1) * 8);
+    alloc((void **)&s->plan, (size_t)s->kcap * 8);
+    alloc((void **)&s->off, (size_t)(s->kcap + 1) * 8);
+    alloc((void **)&s->d_count, 8);
     alloc((void **)&s->boff, (size_t)(nblk + 1) * 8);
     alloc((void **)&s->bcnt, (size_t)nblk * 4);
     alloc((void **)&s->d_inc, 4);
@@ -506,14 +657,12 @@ int read_stats(BBState *s)
 
 int result(BBState *s, int32_t *makespan_out, int32_t *perm_out)
 {
-    int32_t inc = 0;
-    cudaError_t e = cudaMemcpyAsync(&inc, s->d_inc, 4, cudaMemcpyDeviceToHost, s->stream);
-    if (e == cudaSuccess && perm_out && s->have)
+    cudaError_t e = cudaSuccess;
+    if (perm_out && s->have)
         e = cudaMemcpyAsync(perm_out, s->d_perm, sizeof(int32_t) * s->n, cudaMemcpyDeviceToHost,
                             s->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "B&B result");
-    (void)inc;
     if (makespan_out) *makespan_out = s->have ? s->perm_ms : -1;
     return s->have ? FSP_OK : fsp_fail(FSP_ENOTFOUND, "no schedule within the upper bound");
 }
@@ -624,11 +773,12 @@ extern "C" int fsp_bb_pool_size(void *state, int64_t *n)
 extern "C" int64_t fsp_bb_node_bytes(void *state)
 {
     BBState *s = static_cast<BBState *>(state);
-    return s ? (int64_t)s->stride * 2 + 4 : 0;
+    return s ? (int64_t)node_bytes(s) : 0;
 }
 
-// Donor side: the shallowest open nodes (bottom of the stack, largest
-// subtrees) go out as [k][stride] u16 prefixes followed by [k] int32 depths.
+// Donor side: the shallowest open nodes (bottom of the stack, the largest
+// subtrees) go out as one flat buffer of fsp_bb_node_bytes per node:
+// [k][stride] u16 prefixes | [k] depth | [k][m] C | [k] cursor | [k] LB.
 extern "C" int fsp_bb_export(void *state, int64_t max_nodes, void *d_buf, int64_t *n_out)
 {
     BBState *s = static_cast<BBState *>(state);
@@ -637,12 +787,7 @@ extern "C" int fsp_bb_export(void *state, int64_t max_nodes, void *d_buf, int64_
     const int64_t k = std::min(max_nodes, s->size - s->base);
     *n_out = k;
     if (k == 0) return FSP_OK;
-    uint8_t *b = static_cast<uint8_t *>(d_buf);
-    cudaError_t e = cudaMemcpyAsync(b, s->st_pf + (size_t)s->base * s->stride,
-                                    (size_t)k * s->stride * 2, cudaMemcpyDeviceToDevice, s->stream);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(b + (size_t)k * s->stride * 2, s->st_dp + s->base, (size_t)k * 4,
-                            cudaMemcpyDeviceToDevice, s->stream);
+    cudaError_t e = copy_nodes(s, flat_view(s, d_buf, k), 0, s->st, s->base, k);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "export");
     s->base += k;
@@ -655,33 +800,17 @@ extern "C" int fsp_bb_import(void *state, const void *d_buf, int64_t k)
     BBState *s = static_cast<BBState *>(state);
     if (!s || k < 0 || (k > 0 && !d_buf)) return fsp_fail(FSP_EINVAL, "bad import arguments");
     if (k == 0) return FSP_OK;
-    // compact the deque first if the bottom has drifted
-    if (s->base > 0) {
+    cudaError_t e = cudaSuccess;
+    if (s->base > 0) { // compact the deque: move [base, size) down in non-overlapping chunks
         const int64_t open = s->size - s->base;
-        cudaError_t e = cudaSuccess;
-        if (open > 0) {
-            // move in chunks that never overlap destructively (dst < src)
-            for (int64_t q = 0; q < open && e == cudaSuccess; q += s->base) {
-                const int64_t c = std::min(s->base, open - q);
-                e = cudaMemcpyAsync(s->st_pf + (size_t)q * s->stride,
-                                    s->st_pf + (size_t)(s->base + q) * s->stride,
-                                    (size_t)c * s->stride * 2, cudaMemcpyDeviceToDevice, s->stream);
-                if (e == cudaSuccess)
-                    e = cudaMemcpyAsync(s->st_dp + q, s->st_dp + s->base + q, (size_t)c * 4,
-                                        cudaMemcpyDeviceToDevice, s->stream);
-            }
-        }
+        for (int64_t q = 0; q < open && e == cudaSuccess; q += s->base)
+            e = copy_nodes(s, s->st, q, s->st, s->base + q, std::min(s->base, open - q));
         if (e != cudaSuccess) return fsp_cuda_fail(e, "import compaction");
         s->size = open;
         s->base = 0;
     }
     if (s->size + k > s->cap) return fsp_fail(FSP_ENOMEM, "B&B stack full");
-    const uint8_t *b = static_cast<const uint8_t *>(d_buf);
-    cudaError_t e = cudaMemcpyAsync(s->st_pf + (size_t)s->size * s->stride, b,
-                                    (size_t)k * s->stride * 2, cudaMemcpyDeviceToDevice, s->stream);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(s->st_dp + s->size, b + (size_t)k * s->stride * 2, (size_t)k * 4,
-                            cudaMemcpyDeviceToDevice, s->stream);
+    e = copy_nodes(s, s->st, s->size, flat_view(s, d_buf, k), 0, k);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "import");
     s->size += k;

@@ -28,6 +28,7 @@ struct fsp_lb_layout {
     size_t off_ptm, ptm_bytes; // PTM int32 [n][mp4]
     size_t off_bar;            // mbarrier
     size_t off_rt, rt_bytes;   // per warp: R[MAXM][32*npl], T[MAXM][32*npl]
+    size_t off_list, list_bytes; // per warp (sparse walk): compacted records of a couple
     size_t off_tab;            // one couple group: [kl header][records]
     size_t kl_bytes, group_bytes;
 };
@@ -37,6 +38,7 @@ struct fsp_lb_plan {
     bool exact;          // maxm == m (5, 10, 20)
     bool s16;            // 16-bit walk (records in the s16 meta form)
     int npl;             // nodes per lane (2 or 4): U rows are 4*npl bytes per warp
+    bool sparse;         // walk only the records of jobs live in the warp (B&B pools)
     uint32_t smem_base;  // shared-window address of dynamic smem offset 0
     int nrec;            // records per couple (n rounded up to even)
     fsp_lb_layout L;
@@ -62,7 +64,9 @@ struct fsp_instance {
     int32_t *d_ptm32;    // [n][m] int32 (B&B)
     int *d_err;          // malformed-node flag
     int64_t table_bytes;
-    fsp_lb_plan plan;
+    fsp_lb_plan plan;    // arbitrary pools (dense walk)
+    fsp_lb_plan plan_bb; // B&B child pools (sparse walk, completion times supplied)
+    uint8_t *d_tables_bb; // tables laid out for plan_bb
     // host-API staging (lazily created, guarded by a mutex in api.cu)
     void *host_ctx;
 };
@@ -72,10 +76,13 @@ int fsp_fail(int code, const std::string &msg);
 int fsp_cuda_fail(cudaError_t e, const char *what);
 
 // lb kernel launch (lb_kernel.cu)
-int fsp_plan_lb(fsp_instance *inst);
+int fsp_plan_lb(fsp_instance *inst, bool sparse);
 int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                   const int32_t *depth, int64_t pool, int32_t *lb_out, cudaStream_t s);
 // same, pool size read on the device from *pool_dev when pool_dev != nullptr
+// and, optionally, the nodes' completion times cin [pool][cin_stride] and the
+// sparse-walk plan (B&B child pools)
 int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                       const int32_t *depth, int64_t pool, const int64_t *pool_dev,
-                      int32_t *lb_out, cudaStream_t s);
+                      const int32_t *cin, int32_t cin_stride, bool sparse, int32_t *lb_out,
+                      cudaStream_t s);

@@ -19,47 +19,11 @@
 
 #include "fsp_internal.h"
 
-extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_instance **out)
+// Per-couple records in the layout of plan `pl` (groups, U addresses, walk form):
+// [u32 (k | l<<16) x ppg][fsp_rec x np x nrec][slack] per group.
+static void build_tables(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl,
+                         std::vector<uint8_t> &blob)
 {
-    if (!ptm || !out) return fsp_fail(FSP_EINVAL, "null pointer");
-    *out = nullptr;
-    if (n < 1 || m < 2) return fsp_fail(FSP_EINVAL, "need n >= 1 and m >= 2");
-    if (n > FSP_MAX_JOBS) return fsp_fail(FSP_ERANGE, "n > FSP_MAX_JOBS");
-    if (m > FSP_MAX_MACHINES) return fsp_fail(FSP_ERANGE, "m > FSP_MAX_MACHINES");
-    int64_t maxp = 0;
-    for (int64_t i = 0; i < (int64_t)n * m; ++i) {
-        if (ptm[i] < 0) return fsp_fail(FSP_EINVAL, "negative processing time");
-        maxp = std::max<int64_t>(maxp, ptm[i]);
-    }
-    if (maxp > 32767) return fsp_fail(FSP_ERANGE, "processing time > 32767");
-    if ((int64_t)(n + m - 1) * maxp >= INT32_MAX)
-        return fsp_fail(FSP_ERANGE, "(n+m-1)*max p overflows int32");
-
-    fsp_instance *inst = new (std::nothrow) fsp_instance();
-    if (!inst) return fsp_fail(FSP_ENOMEM, "host allocation");
-    inst->n = n;
-    inst->m = m;
-    inst->P = m * (m - 1) / 2;
-    inst->max_p = (int)maxp;
-    cudaError_t e = cudaGetDevice(&inst->device);
-    if (e != cudaSuccess) {
-        delete inst;
-        return fsp_cuda_fail(e, "cudaGetDevice");
-    }
-    inst->h_ptm = new (std::nothrow) int32_t[(size_t)n * m];
-    if (!inst->h_ptm) {
-        delete inst;
-        return fsp_fail(FSP_ENOMEM, "host allocation");
-    }
-    std::memcpy(inst->h_ptm, ptm, sizeof(int32_t) * (size_t)n * m);
-
-    int rc = fsp_plan_lb(inst);
-    if (rc != FSP_OK) {
-        fsp_instance_free(inst);
-        return rc;
-    }
-    const fsp_lb_plan &pl = inst->plan;
-
     // ---- couple tables, grouped: [u32 (k | l<<16) x ppg][fsp_rec x np x nrec] ----
     std::vector<int32_t> S((size_t)n * (m + 1));
     for (int j = 0; j < n; ++j) {
@@ -73,7 +37,7 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
     auto uaddr = [&](int j) {
         return (uint32_t)(pl.smem_base + pl.L.off_u + (size_t)j * 4 * pl.npl * pl.warps);
     };
-    std::vector<uint8_t> blob(gbytes * pl.groups, 0);
+    blob.assign(gbytes * pl.groups, 0);
     for (int g = 0; g < pl.groups; ++g) { // every record slot starts as padding
         fsp_rec *rec = reinterpret_cast<fsp_rec *>(blob.data() + (size_t)g * gbytes + kl_bytes);
         const size_t nslots = (gbytes - kl_bytes) / sizeof(fsp_rec);
@@ -113,6 +77,52 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
             }
         }
     }
+}
+
+extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_instance **out)
+{
+    if (!ptm || !out) return fsp_fail(FSP_EINVAL, "null pointer");
+    *out = nullptr;
+    if (n < 1 || m < 2) return fsp_fail(FSP_EINVAL, "need n >= 1 and m >= 2");
+    if (n > FSP_MAX_JOBS) return fsp_fail(FSP_ERANGE, "n > FSP_MAX_JOBS");
+    if (m > FSP_MAX_MACHINES) return fsp_fail(FSP_ERANGE, "m > FSP_MAX_MACHINES");
+    int64_t maxp = 0;
+    for (int64_t i = 0; i < (int64_t)n * m; ++i) {
+        if (ptm[i] < 0) return fsp_fail(FSP_EINVAL, "negative processing time");
+        maxp = std::max<int64_t>(maxp, ptm[i]);
+    }
+    if (maxp > 32767) return fsp_fail(FSP_ERANGE, "processing time > 32767");
+    if ((int64_t)(n + m - 1) * maxp >= INT32_MAX)
+        return fsp_fail(FSP_ERANGE, "(n+m-1)*max p overflows int32");
+
+    fsp_instance *inst = new (std::nothrow) fsp_instance();
+    if (!inst) return fsp_fail(FSP_ENOMEM, "host allocation");
+    inst->n = n;
+    inst->m = m;
+    inst->P = m * (m - 1) / 2;
+    inst->max_p = (int)maxp;
+    cudaError_t e = cudaGetDevice(&inst->device);
+    if (e != cudaSuccess) {
+        delete inst;
+        return fsp_cuda_fail(e, "cudaGetDevice");
+    }
+    inst->h_ptm = new (std::nothrow) int32_t[(size_t)n * m];
+    if (!inst->h_ptm) {
+        delete inst;
+        return fsp_fail(FSP_ENOMEM, "host allocation");
+    }
+    std::memcpy(inst->h_ptm, ptm, sizeof(int32_t) * (size_t)n * m);
+
+    int rc = fsp_plan_lb(inst, false);
+    if (rc == FSP_OK) rc = fsp_plan_lb(inst, true);
+    if (rc != FSP_OK) {
+        fsp_instance_free(inst);
+        return rc;
+    }
+    const fsp_lb_plan &pl = inst->plan;
+    std::vector<uint8_t> blob, blob_bb;
+    build_tables(ptm, n, m, inst->plan, blob);
+    build_tables(ptm, n, m, inst->plan_bb, blob_bb);
 
     // ---- PTM as int32 rows padded to mp4 (16-byte rows) for shared memory ----
     const int mp4 = (m + 3) & ~3;
@@ -122,6 +132,9 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
 
     inst->table_bytes = (int64_t)blob.size();
     e = cudaMalloc(&inst->d_tables, blob.size());
+    if (e == cudaSuccess) e = cudaMalloc(&inst->d_tables_bb, blob_bb.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(inst->d_tables_bb, blob_bb.data(), blob_bb.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&inst->d_ptm32s, pl.L.ptm_bytes);
     if (e == cudaSuccess) e = cudaMalloc(&inst->d_ptm32, sizeof(int32_t) * (size_t)n * m);
     if (e == cudaSuccess) e = cudaMalloc(&inst->d_err, sizeof(int));
@@ -147,6 +160,7 @@ extern "C" void fsp_instance_free(fsp_instance *inst)
     if (!inst) return;
     if (inst->host_ctx) fsp_host_ctx_free(inst->host_ctx);
     if (inst->d_tables) cudaFree(inst->d_tables);
+    if (inst->d_tables_bb) cudaFree(inst->d_tables_bb);
     if (inst->d_ptm32s) cudaFree(inst->d_ptm32s);
     if (inst->d_ptm32) cudaFree(inst->d_ptm32);
     if (inst->d_err) cudaFree(inst->d_err);

@@ -101,6 +101,8 @@ struct LbArgs {
     int n, m, P, mp4, nrec;
     int stride;
     uint32_t hi_mul;       // 0x10000 (see mask_addr)
+    const int32_t *cin;    // optional prefix completion times [pool][cin_stride]
+    int cin_stride;
 };
 
 // Shared address of U[job][warp] from a record's meta word (wst = 4*NPL*warp).
@@ -166,7 +168,7 @@ __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1
             upd<S16>((MASK).b[q_], lanebit, (C1), (META), uu[q_], ww[q_]);      \
     }
 
-template <int MAXM, bool EXACT, bool S16, int NPL>
+template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE>
 __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbArgs a)
 {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -184,6 +186,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     rt_t *Rs = reinterpret_cast<rt_t *>(smem + a.L.off_rt + (size_t)warp * a.L.rt_bytes);
     rt_t *Ts = Rs + MAXM * TN;
     uint8_t *s_tab = smem + a.L.off_tab;
+    // SPARSE: per-warp list of the couple's records whose job is unscheduled in
+    // at least one of the warp's nodes (the walk over the others is a no-op)
+    uint2 *s_list = reinterpret_cast<uint2 *>(smem + a.L.off_list + (size_t)warp * a.L.list_bytes);
 
     if (smem_u32(smem) != a.smem_base) { // records carry absolute shared addresses
         if (threadIdx.x == 0) atomicOr(a.err, 2);
@@ -265,6 +270,22 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
             }
         }
 
+        // live jobs: unscheduled in at least one node of this warp
+        int live = n;
+        if constexpr (SPARSE) {
+            live = 0;
+            for (int j0 = 0; j0 < n; j0 += 32) {
+                const int j = j0 + lane;
+                uint32_t any = 0;
+                if (j < n) {
+#pragma unroll
+                    for (int q = 0; q < NPL; ++q) any |= Uw[(j * W + warp) * NPL + q];
+                }
+                live += __popc(__ballot_sync(0xffffffffu, any != 0));
+            }
+        }
+        const bool compact = SPARSE && live + 16 <= n;
+
         // ---------------- per node of this lane: C, heads, tails ----------------
 #pragma unroll 1
         for (int q = 0; q < NPL; ++q) {
@@ -278,7 +299,14 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
 #pragma unroll
             for (int k = 0; k < MAXM; ++k) C[k] = 0;
             const uint16_t *row = a.prefix + (size_t)(d ? node : 0) * a.stride;
-            for (int i = 0; i < d; ++i) {
+            if (a.cin) { // completion times supplied (B&B children: parent C + one job)
+                if (node < pool) {
+#pragma unroll
+                    for (int k = 0; k < MAXM; ++k)
+                        if (k < m) C[k] = a.cin[(size_t)node * a.cin_stride + k];
+                }
+            }
+            for (int i = 0; i < (a.cin ? 0 : d); ++i) {
                 uint32_t job = row[i];
                 if (job >= (uint32_t)n) { bad = true; job = 0; }
                 const int4 *pr = reinterpret_cast<const int4 *>(s_ptm + job * a.mp4);
@@ -400,6 +428,37 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                     ww[q] = Rs[k * TN + q * 32 + lane];
                 }
                 const uint4 *rp = recs + (size_t)pl * n2;
+                int n4c = n4;
+                if constexpr (SPARSE) {
+                    if (compact) {
+                        // keep the records whose job is live, in JM order
+                        const uint2 *col = reinterpret_cast<const uint2 *>(rp);
+                        int cnt = 0;
+                        for (int i0 = 0; i0 < a.nrec; i0 += 32) {
+                            const int i = i0 + lane;
+                            uint2 r = make_uint2(0u, 0u);
+                            bool lv = false;
+                            if (i < a.nrec) {
+                                r = col[i];
+                                const Mask<NPL> mk = FSP_MASK(r.y);
+                                uint32_t any = 0;
+#pragma unroll
+                                for (int q = 0; q < NPL; ++q) any |= mk.b[q];
+                                lv = any != 0;
+                            }
+                            const uint32_t bal = __ballot_sync(0xffffffffu, lv);
+                            if (lv) s_list[cnt + __popc(bal & ((1u << lane) - 1u))] = r;
+                            cnt += __popc(bal);
+                        }
+                        // pad to a whole step + the look-ahead slack with no-op records
+                        const uint2 dummy = reinterpret_cast<const uint2 *>(recs)[(size_t)np * a.nrec];
+                        const int cnt4 = (cnt + 3) & ~3;
+                        for (int t = cnt + lane; t < cnt4 + FSP_REC_SLACK; t += 32) s_list[t] = dummy;
+                        __syncwarp();
+                        rp = reinterpret_cast<const uint4 *>(s_list);
+                        n4c = cnt4 >> 2;
+                    }
+                }
                 // lines 08-17, software-pipelined 4 positions per step: records
                 // two steps ahead, U masks one step ahead (the group blob ends
                 // with padding records so the look-ahead stays in bounds).
@@ -409,7 +468,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                 Mask<NPL> mx0 = FSP_MASK(xa.y), mx1 = FSP_MASK(xa.w);
                 Mask<NPL> mx2 = FSP_MASK(xb.y), mx3 = FSP_MASK(xb.w);
                 int s = 0;
-                for (; s + 2 <= n4; s += 2) {
+                for (; s + 2 <= n4c; s += 2) {
                     const Mask<NPL> my0 = FSP_MASK(ya.y), my1 = FSP_MASK(ya.w);
                     const Mask<NPL> my2 = FSP_MASK(yb.y), my3 = FSP_MASK(yb.w);
                     FSP_UPD(mx0, xa.x, xa.y);
@@ -429,7 +488,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                     ya = rp[2 * s + 6];
                     yb = rp[2 * s + 7];
                 }
-                if (s < n4) { // odd number of steps: the last one is in X
+                if (s < n4c) { // odd number of steps: the last one is in X
                     FSP_UPD(mx0, xa.x, xa.y);
                     FSP_UPD(mx1, xa.z, xa.w);
                     FSP_UPD(mx2, xb.x, xb.y);
@@ -442,6 +501,8 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
 #pragma unroll
                 for (int q = 0; q < NPL; ++q) // lines 18-19
                     lb[q] = max(lb[q], uu[q] + Ts[l * TN + q * 32 + lane]);
+                if constexpr (SPARSE)
+                    if (compact) __syncwarp(); // the next couple rewrites s_list
             }
         }
 #pragma unroll
@@ -459,27 +520,25 @@ __global__ void smem_base_probe(uint32_t *out)
     *out = smem_u32(smem);
 }
 
-template <int MAXM, bool EXACT, bool S16, int NPL>
-int launch(const fsp_instance *inst, const LbArgs &a, cudaStream_t s)
+template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE>
+int launch(const fsp_lb_plan &pl, const LbArgs &a, cudaStream_t s)
 {
-    const fsp_lb_plan &pl = inst->plan;
-    lb_kernel<MAXM, EXACT, S16, NPL><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
+    lb_kernel<MAXM, EXACT, S16, NPL, SPARSE><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, "lb_kernel launch");
 }
 
-template <int MAXM, bool EXACT, bool S16, int NPL>
-int configure(fsp_instance *inst)
+template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE>
+int configure(fsp_lb_plan &pl)
 {
-    fsp_lb_plan &pl = inst->plan;
     // the attribute is per kernel variant and shared by every instance: set it
     // to the device's opt-in maximum, never to this plan's size
-    cudaError_t e = cudaFuncSetAttribute(lb_kernel<MAXM, EXACT, S16, NPL>,
+    cudaError_t e = cudaFuncSetAttribute(lb_kernel<MAXM, EXACT, S16, NPL, SPARSE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          pl.smem_optin);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "cudaFuncSetAttribute");
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM, EXACT, S16, NPL>,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM, EXACT, S16, NPL, SPARSE>,
                                                       pl.warps * 32, pl.smem_bytes);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "occupancy");
     if (per_sm < 1) return fsp_fail(FSP_ERANGE, "lb kernel does not fit on an SM");
@@ -488,20 +547,25 @@ int configure(fsp_instance *inst)
     return FSP_OK;
 }
 
-// (MAXM, EXACT, S16, NPL) specialisations: exact m for Taillard's 5/10/20
-// machines (with 2 or 4 nodes per lane), generic m with 2 nodes per lane.
+// (MAXM, EXACT, S16, NPL, SPARSE) specialisations: exact m for Taillard's
+// 5/10/20 machines (2 or 4 nodes per lane, dense or sparse walk), generic m
+// with 2 nodes per lane and the dense walk.
+#define FSP_EXACT_CASE(M, FN, S, ...)                                           \
+    case M * 2 + 1:                                                             \
+        if (pl.sparse)                                                          \
+            return pl.npl == 4 ? FN<M, true, S, 4, true>(__VA_ARGS__)           \
+                               : FN<M, true, S, 2, true>(__VA_ARGS__);          \
+        return pl.npl == 4 ? FN<M, true, S, 4, false>(__VA_ARGS__)              \
+                           : FN<M, true, S, 2, false>(__VA_ARGS__);
 #define FSP_DISPATCH_M(FN, S, ...)                                              \
     switch (pl.maxm * 2 + (pl.exact ? 1 : 0)) {                                 \
-    case 5 * 2 + 1:                                                             \
-        return pl.npl == 4 ? FN<5, true, S, 4>(__VA_ARGS__) : FN<5, true, S, 2>(__VA_ARGS__); \
-    case 10 * 2 + 1:                                                            \
-        return pl.npl == 4 ? FN<10, true, S, 4>(__VA_ARGS__) : FN<10, true, S, 2>(__VA_ARGS__); \
-    case 20 * 2 + 1:                                                            \
-        return pl.npl == 4 ? FN<20, true, S, 4>(__VA_ARGS__) : FN<20, true, S, 2>(__VA_ARGS__); \
-    case 8 * 2: return FN<8, false, S, 2>(__VA_ARGS__);                         \
-    case 16 * 2: return FN<16, false, S, 2>(__VA_ARGS__);                       \
-    case 24 * 2: return FN<24, false, S, 2>(__VA_ARGS__);                       \
-    default: return FN<32, false, S, 2>(__VA_ARGS__);                           \
+        FSP_EXACT_CASE(5, FN, S, __VA_ARGS__)                                   \
+        FSP_EXACT_CASE(10, FN, S, __VA_ARGS__)                                  \
+        FSP_EXACT_CASE(20, FN, S, __VA_ARGS__)                                  \
+    case 8 * 2: return FN<8, false, S, 2, false>(__VA_ARGS__);                  \
+    case 16 * 2: return FN<16, false, S, 2, false>(__VA_ARGS__);                \
+    case 24 * 2: return FN<24, false, S, 2, false>(__VA_ARGS__);                \
+    default: return FN<32, false, S, 2, false>(__VA_ARGS__);                    \
     }
 #define FSP_DISPATCH(FN, ...)                                                   \
     if (pl.s16) {                                                               \
@@ -515,10 +579,9 @@ int configure(fsp_instance *inst)
 static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 // Set the kernel variant's dynamic-smem attribute and fill ctas_per_sm / grid.
-static int occupancy_of(fsp_instance *inst)
+static int occupancy_of(fsp_lb_plan &pl)
 {
-    const fsp_lb_plan &pl = inst->plan;
-    FSP_DISPATCH(configure, inst);
+    FSP_DISPATCH(configure, pl);
     return FSP_OK;
 }
 
@@ -540,11 +603,12 @@ static int probe_smem_base(uint32_t *base)
 // Choose the machine specialisation, warps per CTA and couple groups so that
 // one couple group + PTM + U + per-warp scratch fit the opt-in shared memory
 // and every U address fits the 16-bit record field.
-int fsp_plan_lb(fsp_instance *inst)
+int fsp_plan_lb(fsp_instance *inst, bool sparse)
 {
-    fsp_lb_plan &pl = inst->plan;
+    fsp_lb_plan &pl = sparse ? inst->plan_bb : inst->plan;
     const int n = inst->n, m = inst->m, P = inst->P;
     pl.exact = (m == 5 || m == 10 || m == 20);
+    pl.sparse = sparse && pl.exact; // sparse walk: exact-m specialisations only
     // 16-bit walk when every walk value fits int16: t2 <= (n+m-1)*max p and
     // w >= -n*max p
     pl.s16 = (int64_t)(n + m - 1) * inst->max_p <= 32767 && (int64_t)n * inst->max_p <= 32767;
@@ -592,7 +656,9 @@ int fsp_plan_lb(fsp_instance *inst)
             L.off_bar = L.off_ptm + L.ptm_bytes;
             L.rt_bytes = 2 * (size_t)pl.maxm * 32 * npl * (pl.s16 ? 2 : 4);
             L.off_rt = L.off_bar + 16;
-            L.off_tab = align16(L.off_rt + (size_t)W * L.rt_bytes);
+            L.list_bytes = pl.sparse ? align16(((size_t)pl.nrec + FSP_REC_SLACK + 4) * 8) : 0;
+            L.off_list = align16(L.off_rt + (size_t)W * L.rt_bytes);
+            L.off_tab = align16(L.off_list + (size_t)W * L.list_bytes);
             for (int G = 1; G <= P; ++G) {
                 const int ppg = (P + G - 1) / G;
                 const int Greal = (P + ppg - 1) / ppg;
@@ -609,14 +675,12 @@ int fsp_plan_lb(fsp_instance *inst)
                     c.pairs_per_group = ppg;
                     c.warps = W;
                     c.smem_bytes = L.off_tab + gb;
-                    fsp_instance tmp = *inst;
-                    tmp.plan = c;
-                    if (occupancy_of(&tmp) == FSP_OK && tmp.plan.ctas_per_sm > 0) {
-                        const double score = (double)W * tmp.plan.ctas_per_sm *
-                                             (npl == 4 ? 1.3 : 1.0) / (1.0 + 0.015 * (Greal - 1));
+                    if (occupancy_of(c) == FSP_OK && c.ctas_per_sm > 0) {
+                        const double score = (double)W * c.ctas_per_sm * (npl == 4 ? 1.3 : 1.0) /
+                                             (1.0 + 0.015 * (Greal - 1));
                         if (score > best) {
                             best = score;
-                            bestp = tmp.plan;
+                            bestp = c;
                         }
                     }
                     break; // more groups only cost for this (npl, W)
@@ -627,7 +691,7 @@ int fsp_plan_lb(fsp_instance *inst)
     }
     if (best > 0) {
         pl = bestp;
-        return occupancy_of(inst); // sets the attribute for the chosen variant
+        return occupancy_of(pl); // sets the attribute for the chosen variant
     }
     return fsp_fail(FSP_ERANGE, "instance tables do not fit in shared memory");
 }
@@ -635,17 +699,21 @@ int fsp_plan_lb(fsp_instance *inst)
 int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                   const int32_t *depth, int64_t pool, int32_t *lb_out, cudaStream_t s)
 {
-    return fsp_launch_lb_dev(inst, prefix, stride, depth, pool, nullptr, lb_out, s);
+    return fsp_launch_lb_dev(inst, prefix, stride, depth, pool, nullptr, nullptr, 0, false, lb_out, s);
 }
 
 int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                       const int32_t *depth, int64_t pool, const int64_t *pool_dev,
-                      int32_t *lb_out, cudaStream_t s)
+                      const int32_t *cin, int32_t cin_stride, bool sparse, int32_t *lb_out,
+                      cudaStream_t s)
 {
-    const fsp_lb_plan &pl = inst->plan;
+    const fsp_lb_plan &pl = sparse ? inst->plan_bb : inst->plan;
+    const uint8_t *tables = sparse ? inst->d_tables_bb : inst->d_tables;
     LbArgs a;
-    a.tables = inst->d_tables;
+    a.tables = tables;
     a.ptm = inst->d_ptm32s;
+    a.cin = cin;
+    a.cin_stride = cin_stride;
     a.prefix = prefix;
     a.depth = depth;
     a.lb_out = lb_out;
@@ -663,5 +731,5 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.nrec = pl.nrec;
     a.stride = stride;
     a.hi_mul = 0x10000u;
-    FSP_DISPATCH(launch, inst, a, s);
+    FSP_DISPATCH(launch, pl, a, s);
 }

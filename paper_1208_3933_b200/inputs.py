@@ -115,3 +115,41 @@ def pool_fixed_depth(n: int, N: int, d: int, seed: int, stride: int | None = Non
 
 def pool_seed(config_name: str) -> int:
     return POOL_SEED_BASE + CONFIGS.index(config_name)
+
+
+def pool_children(n: int, parent_pf: np.ndarray, parent_dp: np.ndarray, stride: int | None = None):
+    """B&B-shaped pool: every child (prefix + j, j unscheduled, ascending j) of
+    each parent, parents in order, children contiguous (the layout of the
+    device B&B's child pools)."""
+    stride = default_stride(n) if stride is None else stride
+    rows, deps = [], []
+    for pf, d in zip(parent_pf, parent_dp):
+        d = int(d)
+        used = set(int(x) for x in pf[:d])
+        for j in range(n):
+            if j in used:
+                continue
+            r = np.full(stride, 0xFFFF, dtype=np.uint16)
+            r[:d] = pf[:d]
+            r[d] = j
+            rows.append(r)
+            deps.append(d + 1)
+    if not rows:
+        return np.zeros((0, stride), np.uint16), np.zeros(0, np.int32)
+    return np.stack(rows), np.array(deps, dtype=np.int32)
+
+
+def pool_dfs_frontier(n: int, n_parents: int, depth: int, seed: int, stride: int | None = None):
+    """Children of `n_parents` parents that share a random prefix of length
+    depth-1 and differ in their last job (siblings and cousins, as in a
+    depth-first batch)."""
+    base, _ = pool_fixed_depth(n, 1, max(depth - 1, 0), seed, stride)
+    d0 = max(depth - 1, 0)
+    used = set(int(x) for x in base[0, :d0])
+    free = [j for j in range(n) if j not in used]
+    rng = np.random.default_rng(seed)
+    pick = rng.permutation(free)[:n_parents]
+    par = np.repeat(base, len(pick), axis=0)
+    for i, j in enumerate(pick):
+        par[i, d0] = j
+    return pool_children(n, par, np.full(len(pick), d0 + 1, np.int32), stride)

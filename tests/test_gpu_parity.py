@@ -169,3 +169,50 @@ def test_full_size_200x20_sampled(torch, fsp, orc):
     assert (got[sample] == want).all()
     # properties at any size: LB >= prefix-free machine bound, <= (n+m-1)*max p
     assert got.min() >= int(ptm.sum(0).max()) and got.max() <= (n + m - 1) * int(ptm.max())
+
+
+# ------------------------------------------------ sibling (B&B child) pools
+
+def completion_times(p, pf, dp):
+    """C_k of each prefix by event simulation (independent of both sides)."""
+    m = p.shape[1]
+    out = np.zeros((len(dp), m), np.int32)
+    for i in range(len(dp)):
+        C = [0] * m
+        for j in pf[i, :dp[i]]:
+            prev = 0
+            for k in range(m):
+                C[k] = max(C[k], prev) + int(p[j, k])
+                prev = C[k]
+        out[i] = C
+    return out
+
+
+@pytest.mark.parametrize("name,depth", [("ta021", 15), ("ta051", 40), ("ta091", 190),
+                                        ("ta091", 120), ("ta001", 10), ("ta111", 480)])
+def test_parity_sibling_pools(torch, fsp, orc, name, depth):
+    n, m, seed = inputs.TAILLARD_SEEDS[name]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_dfs_frontier(n, 40, depth, depth)
+    inst = fsp.Instance(ptm)
+    want = orc.Tables(ptm).lb_eval(pf, dp)
+    for comp in (False, True):
+        C = torch.from_numpy(completion_times(ptm, pf, dp)).cuda() if comp else None
+        got = inst.lb_eval_sibling(dev(torch, pf), dev(torch, dp), C)
+        torch.cuda.synchronize()
+        got = got.cpu().numpy()
+        assert inst.check() == fsp.FSP_OK
+        assert (got == want).all(), (name, depth, comp, int((got != want).sum()))
+
+
+def test_parity_sibling_api_on_random_pools(torch, fsp, orc):
+    """The sparse plan on D1 pools (compaction rarely applies) and on deep
+    random pools (it does) still equals the oracle."""
+    for name, N in (("ta021", 3001), ("ta091", 1031)):
+        n, m, seed = inputs.TAILLARD_SEEDS[name]
+        ptm = inputs.taillard(n, m, seed)
+        inst = fsp.Instance(ptm)
+        T = orc.Tables(ptm)
+        for pf, dp in (inputs.pool_d1(n, N, 9), inputs.pool_fixed_depth(n, N, n - 3, 10)):
+            got = inst.lb_eval_sibling(dev(torch, pf), dev(torch, dp)).cpu().numpy()
+            assert (got == T.lb_eval(pf, dp)).all()
