@@ -9,7 +9,8 @@
 #include "fsp.h"
 
 // Per-(couple, position) record of the pair walk, staged in shared memory.
-//   c1   = p_{j,k} + lag_j(k,l)  = sum_{k<=i<l} p_{j,i}        (int32)
+//   c1   = p_{j,k} + lag_j(k,l)  = sum_{k<=i<l} p_{j,i}        (int32; s16 walk:
+//          low half, job id j in the high half)
 //   meta = (c2 << 16) | addr_j   (int32 walk)  or  (addr_j << 16) | (c2 & 0xffff) (s16 walk)
 //   c2 = p_{j,k} - p_{j,l} (int16); addr_j = shared-window address of U[j][warp 0]
 // j is the job at this position of the couple's Johnson-with-lags order.

@@ -42,7 +42,7 @@ static void build_tables(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl
         fsp_rec *rec = reinterpret_cast<fsp_rec *>(blob.data() + (size_t)g * gbytes + kl_bytes);
         const size_t nslots = (gbytes - kl_bytes) / sizeof(fsp_rec);
         for (size_t i = 0; i < nslots; ++i) {
-            rec[i].c1 = 0;
+            rec[i].c1 = pl.s16 ? (int32_t)((uint32_t)n << 16) : 0; // job id n: never live
             rec[i].meta = pl.s16 ? (int32_t)(uaddr(n) << 16) : (int32_t)uaddr(n);
         }
     }
@@ -71,7 +71,9 @@ static void build_tables(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl
             for (int i = 0; i < n; ++i) {
                 const int j = order[i];
                 const int c2 = ptm[(size_t)j * m + k] - ptm[(size_t)j * m + l];
-                rec[i].c1 = A[j];
+                // s16 walk: c1 < 2^15 in the low half, the job id in the high
+                // half (read by the sparse walk's compaction only)
+                rec[i].c1 = pl.s16 ? (int32_t)(((uint32_t)j << 16) | (uint32_t)A[j]) : A[j];
                 rec[i].meta = pl.s16 ? (int32_t)((uaddr(j) << 16) | ((uint32_t)c2 & 0xffffu))
                                      : (int32_t)(((uint32_t)c2 << 16) | uaddr(j));
             }

@@ -270,8 +270,10 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
             }
         }
 
-        // live jobs: unscheduled in at least one node of this warp
+        // live jobs: unscheduled in at least one node of this warp; lane w keeps
+        // the bitset word of jobs 32w .. 32w+31 (n <= 1024 for the sparse plan)
         int live = n;
+        uint32_t livew = 0;
         if constexpr (SPARSE) {
             live = 0;
             for (int j0 = 0; j0 < n; j0 += 32) {
@@ -281,7 +283,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
 #pragma unroll
                     for (int q = 0; q < NPL; ++q) any |= Uw[(j * W + warp) * NPL + q];
                 }
-                live += __popc(__ballot_sync(0xffffffffu, any != 0));
+                const uint32_t bal = __ballot_sync(0xffffffffu, any != 0);
+                if (lane == (j0 >> 5)) livew = bal;
+                live += __popc(bal);
             }
         }
         const bool compact = SPARSE && live + 16 <= n;
@@ -437,15 +441,12 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                         for (int i0 = 0; i0 < a.nrec; i0 += 32) {
                             const int i = i0 + lane;
                             uint2 r = make_uint2(0u, 0u);
-                            bool lv = false;
-                            if (i < a.nrec) {
-                                r = col[i];
-                                const Mask<NPL> mk = FSP_MASK(r.y);
-                                uint32_t any = 0;
-#pragma unroll
-                                for (int q = 0; q < NPL; ++q) any |= mk.b[q];
-                                lv = any != 0;
-                            }
+                            if (i < a.nrec) r = col[i];
+                            // s16 records carry the job in the top half of c1
+                            // (the walk's 16x2 ops ignore that half)
+                            const uint32_t j = r.x >> 16;
+                            const uint32_t word = __shfl_sync(0xffffffffu, livew, (j >> 5) & 31);
+                            const bool lv = i < a.nrec && ((word >> (j & 31)) & 1u);
                             const uint32_t bal = __ballot_sync(0xffffffffu, lv);
                             if (lv) s_list[cnt + __popc(bal & ((1u << lane) - 1u))] = r;
                             cnt += __popc(bal);
@@ -608,11 +609,13 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     fsp_lb_plan &pl = sparse ? inst->plan_bb : inst->plan;
     const int n = inst->n, m = inst->m, P = inst->P;
     pl.exact = (m == 5 || m == 10 || m == 20);
-    pl.sparse = sparse && pl.exact; // sparse walk: exact-m specialisations only
     // 16-bit walk when every walk value fits int16: t2 <= (n+m-1)*max p and
     // w >= -n*max p
     pl.s16 = (int64_t)(n + m - 1) * inst->max_p <= 32767 && (int64_t)n * inst->max_p <= 32767;
     if (const char *s = getenv("FSP_LB_S16")) pl.s16 = pl.s16 && atoi(s) != 0;
+    // sparse walk: exact-m s16 specialisations (records carry the job id),
+    // 64 <= n <= 1024 (below 64 jobs the compaction does not pay: measured)
+    pl.sparse = sparse && pl.exact && pl.s16 && n >= 64 && n <= 1024;
     if (pl.exact) pl.maxm = m;
     else if (m <= 8) pl.maxm = 8;
     else if (m <= 16) pl.maxm = 16;
@@ -638,6 +641,8 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     // reload).  Env FSP_LB_NPL / FSP_LB_WARPS pin a choice (sweeps, tests).
     int npl_lo = 2, npl_hi = pl.exact ? 4 : 2;
     if (const char *s = getenv("FSP_LB_NPL")) npl_lo = npl_hi = (atoi(s) == 4 && pl.exact) ? 4 : 2;
+    // sparse walk: 64-node warps keep the union of the block's unscheduled sets small
+    if (pl.sparse) npl_lo = npl_hi = getenv("FSP_BB_NPL") && atoi(getenv("FSP_BB_NPL")) == 4 ? 4 : 2;
     int w_lo = 1, w_hi = pl.maxm > 20 ? 8 : 16; // launch bounds of the wide variants
     if (const char *s = getenv("FSP_LB_WARPS")) w_lo = w_hi = std::max(1, std::min(w_hi, atoi(s)));
     double best = -1.0;

@@ -45,9 +45,9 @@ if __name__ == "__main__":
     cfgs = sys.argv[1:] or ["ta091"]
     for c in cfgs:
         name, N = (c.split(":") + ["1048576"])[:2]
-        for npl in os.environ.get("SWEEP_NPL", "2,4").split(","):
+        for npl in os.environ.get("SWEEP_NPL", "0").split(","):
             os.environ["FSP_LB_NPL"] = npl
-            for w in ([int(x) for x in os.environ.get("SWEEP_WARPS", "16,8").split(",")]):
+            for w in ([int(x) for x in os.environ.get("SWEEP_WARPS", "0").split(",")]):
                 r = time_cfg(name, int(N), w)
                 r["npl_env"] = int(npl)
                 print(json.dumps(r), flush=True)
