@@ -255,18 +255,53 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
         }
         __syncwarp();
         // coalesced pass over the TN prefix records: clear the scheduled bits
+        // (16-byte rows: each lane takes eight job ids per vector load; the
+        // next node's row is loaded while this one's bits are cleared)
+        const bool rows16 = ((reinterpret_cast<uintptr_t>(a.prefix) | ((uintptr_t)a.stride * 2)) & 15) == 0;
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
-            for (int L = 0; L < 32; ++L) {
-                const int dL = __shfl_sync(0xffffffffu, dq[q], L);
-                if (dL == 0) continue;
-                const uint16_t *row = a.prefix + (size_t)(tile * TN + q * 32 + L) * a.stride;
-                const uint32_t clr = ~(1u << L);
-                for (int i = lane; i < dL; i += 32) {
-                    const uint32_t job = row[i];
-                    if (job < (uint32_t)n) Uw[(job * W + warp) * NPL + q] &= clr;
+            if (rows16) {
+                // segment `sg` of node L's row: entries 256*sg .. 256*sg+255
+                auto load_row = [&](int L, int sg) {
+                    const int dL = __shfl_sync(0xffffffffu, dq[q], L);
+                    uint4 v = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                    if (sg * 256 + lane * 8 < dL)
+                        v = reinterpret_cast<const uint4 *>(a.prefix + (size_t)(tile * TN + q * 32 + L) *
+                                                                           a.stride)[sg * 32 + lane];
+                    return v;
+                };
+                // the first segment of the next node is loaded while this
+                // node's bits are cleared
+                uint4 cur = load_row(0, 0);
+                for (int L = 0; L < 32; ++L) {
+                    const int dL = __shfl_sync(0xffffffffu, dq[q], L);
+                    const uint32_t clr = ~(1u << L);
+                    const uint4 nxt = L + 1 < 32 ? load_row(L + 1, 0) : cur;
+                    for (int sg = 0; sg * 256 < dL; ++sg) {
+                        if (sg > 0) cur = load_row(L, sg);
+                        const uint32_t w4[4] = {cur.x, cur.y, cur.z, cur.w};
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            const uint32_t job = (t & 1) ? (w4[t >> 1] >> 16) : (w4[t >> 1] & 0xffffu);
+                            if (sg * 256 + lane * 8 + t < dL && job < (uint32_t)n)
+                                Uw[(job * W + warp) * NPL + q] &= clr;
+                        }
+                    }
+                    __syncwarp();
+                    cur = nxt;
                 }
-                __syncwarp();
+            } else {
+                for (int L = 0; L < 32; ++L) {
+                    const int dL = __shfl_sync(0xffffffffu, dq[q], L);
+                    if (dL == 0) continue;
+                    const uint16_t *row = a.prefix + (size_t)(tile * TN + q * 32 + L) * a.stride;
+                    const uint32_t clr = ~(1u << L);
+                    for (int i = lane; i < dL; i += 32) {
+                        const uint32_t job = row[i];
+                        if (job < (uint32_t)n) Uw[(job * W + warp) * NPL + q] &= clr;
+                    }
+                    __syncwarp();
+                }
             }
         }
 
@@ -310,9 +345,11 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                         if (k < m) C[k] = a.cin[(size_t)node * a.cin_stride + k];
                 }
             }
-            for (int i = 0; i < (a.cin ? 0 : d); ++i) {
-                uint32_t job = row[i];
-                if (job >= (uint32_t)n) { bad = true; job = 0; }
+            auto step = [&](uint32_t job) {
+                if (job >= (uint32_t)n) {
+                    bad = true;
+                    job = 0;
+                }
                 const int4 *pr = reinterpret_cast<const int4 *>(s_ptm + job * a.mp4);
                 int prev = 0;
 #pragma unroll
@@ -330,7 +367,25 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                         }
                     }
                 }
+            };
+            const int dd = a.cin ? 0 : d;
+            int i = 0;
+            // 16-byte rows: eight job ids per vector load
+            if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+                const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
+                for (; i + 8 <= dd; i += 8) {
+                    const uint4 v = r4[i >> 3];
+                    step(v.x & 0xffffu);
+                    step(v.x >> 16);
+                    step(v.y & 0xffffu);
+                    step(v.y >> 16);
+                    step(v.z & 0xffffu);
+                    step(v.z >> 16);
+                    step(v.w & 0xffffu);
+                    step(v.w >> 16);
+                }
             }
+            for (; i < dd; ++i) step(row[i]);
             // a2/a3: r_j0 = C_0, r_jk = max(C_k, r_j,k-1 + p_j,k-1) (R3); R_k =
             // min over unscheduled j (R5); Q_l = min_j q_jl, q_jl = sum_{i>l}
             // p_ji (R4); L_l = sum_j p_jl closes the (u, w) walk.

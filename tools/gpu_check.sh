@@ -1,2 +1,2 @@
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 600 python tools/bb_try.py ta091:2147483647:15 > gpurun_out/bbt.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_bb.py -x -q 2>&1 | tail -2 >> gpurun_out/bbt.txt
