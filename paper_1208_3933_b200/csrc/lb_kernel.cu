@@ -112,9 +112,12 @@ struct LbArgs {
 // the FMA pipe instead of strength-reducing it to an ALU LEA.HI: the ALU pipe
 // is the walk's bottleneck.)
 template <bool S16>
-__device__ __forceinline__ uint32_t mask_addr(uint32_t meta, uint32_t wst, uint32_t hi_mul)
+__device__ __forceinline__ uint32_t mask_addr(uint32_t meta, uint32_t wst, uint32_t hi_mul,
+                                              uint64_t wst64)
 {
-    if constexpr (S16) return __umulhi(meta, hi_mul) + wst;
+    // s16: one IMAD.WIDE.U32 with the loop-invariant 64-bit addend wst << 32
+    // (a 32-bit "hi + c" form makes ptxas rebuild the {0, c} pair every time)
+    if constexpr (S16) return (uint32_t)(((uint64_t)meta * hi_mul + wst64) >> 32);
     else return (meta & 0xffffu) | wst;
 }
 
@@ -161,7 +164,7 @@ __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1
     }
 }
 
-#define FSP_MASK(META) lds_mask<NPL>(mask_addr<S16>((META), wst, hi_mul))
+#define FSP_MASK(META) lds_mask<NPL>(mask_addr<S16>((META), wst, hi_mul, wst64))
 #define FSP_UPD(MASK, C1, META)                                                 \
     {                                                                           \
         _Pragma("unroll") for (int q_ = 0; q_ < NPL; ++q_)                      \
@@ -225,6 +228,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     const uint32_t lanebit = 1u << lane;
     const uint32_t wst = 4u * NPL * warp;
     const uint32_t hi_mul = a.hi_mul;
+    const uint64_t wst64 = (uint64_t)wst << 32;
 
     for (long long chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
         const long long tile = chunk * W + warp;
