@@ -496,19 +496,34 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                     if (compact) {
                         // keep the records whose job is live, in JM order
                         const uint2 *col = reinterpret_cast<const uint2 *>(rp);
+                        // four 32-position chunks per round: loads, live tests and
+                        // ballots of a round are independent; only the stores
+                        // depend on the running count
                         int cnt = 0;
-                        for (int i0 = 0; i0 < a.nrec; i0 += 32) {
-                            const int i = i0 + lane;
-                            uint2 r = make_uint2(0u, 0u);
-                            if (i < a.nrec) r = col[i];
-                            // s16 records carry the job in the top half of c1
-                            // (the walk's 16x2 ops ignore that half)
-                            const uint32_t j = r.x >> 16;
-                            const uint32_t word = __shfl_sync(0xffffffffu, livew, (j >> 5) & 31);
-                            const bool lv = i < a.nrec && ((word >> (j & 31)) & 1u);
-                            const uint32_t bal = __ballot_sync(0xffffffffu, lv);
-                            if (lv) s_list[cnt + __popc(bal & ((1u << lane) - 1u))] = r;
-                            cnt += __popc(bal);
+                        const uint32_t lt = (1u << lane) - 1u;
+                        for (int i0 = 0; i0 < a.nrec; i0 += 128) {
+                            uint2 r[4];
+                            uint32_t bal[4];
+                            bool lv[4];
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                const int i = i0 + 32 * c + lane;
+                                r[c] = i < a.nrec ? col[i] : make_uint2(0u, 0u);
+                            }
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                // s16 records carry the job in the top half of c1
+                                // (the walk's 16x2 ops ignore that half)
+                                const uint32_t j = r[c].x >> 16;
+                                const uint32_t word = __shfl_sync(0xffffffffu, livew, (j >> 5) & 31);
+                                lv[c] = i0 + 32 * c + lane < a.nrec && ((word >> (j & 31)) & 1u);
+                                bal[c] = __ballot_sync(0xffffffffu, lv[c]);
+                            }
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                if (lv[c]) s_list[cnt + __popc(bal[c] & lt)] = r[c];
+                                cnt += __popc(bal[c]);
+                            }
                         }
                         // pad to a whole step + the look-ahead slack with no-op records
                         const uint2 dummy = reinterpret_cast<const uint2 *>(recs)[(size_t)np * a.nrec];
