@@ -25,7 +25,8 @@ struct __align__(8) fsp_rec {
 
 // Dynamic shared-memory layout of the lb kernel (byte offsets).
 struct fsp_lb_layout {
-    size_t off_u, u_bytes;     // U[(n+1)][W][npl] u32 transposed unscheduled sets
+    size_t off_u, u_bytes;     // U[(n+1)][urow_words] u32 transposed unscheduled sets:
+    int urow_words;            //   word warp*npl + q of job j's row = nodes q*32..q*32+31
     size_t off_ptm, ptm_bytes; // PTM int32 [n][mp4]
     size_t off_bar;            // mbarrier
     size_t off_rt, rt_bytes;   // per warp: R[MAXM][32*npl], T[MAXM][32*npl]

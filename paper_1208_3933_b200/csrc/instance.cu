@@ -35,7 +35,7 @@ static void build_tables(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl
     const size_t kl_bytes = pl.L.kl_bytes;
     // shared address of U[j][warp 0]; row n is the always-empty padding row
     auto uaddr = [&](int j) {
-        return (uint32_t)(pl.smem_base + pl.L.off_u + (size_t)j * 4 * pl.npl * pl.warps);
+        return (uint32_t)(pl.smem_base + pl.L.off_u + (size_t)j * 4 * pl.L.urow_words);
     };
     blob.assign(gbytes * pl.groups, 0);
     for (int g = 0; g < pl.groups; ++g) { // every record slot starts as padding

@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     const long long nchunks = (ntiles + W - 1) / W;
     const uint32_t lanebit = 1u << lane;
     const uint32_t wst = 4u * NPL * warp;
+    const int urow = a.L.urow_words; // words per job row of U (padded against bank conflicts)
     const uint32_t hi_mul = a.hi_mul;
     const uint64_t wst64 = (uint64_t)wst << 32;
 
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
         for (int j = lane; j <= n; j += 32) {
 #pragma unroll
             for (int q = 0; q < NPL; ++q) // row n: the padding record's always-empty mask
-                Uw[(j * W + warp) * NPL + q] = j < n ? validq[q] : 0u;
+                Uw[j * urow + warp * NPL + q] = j < n ? validq[q] : 0u;
         }
         __syncwarp();
         // coalesced pass over the TN prefix records: clear the scheduled bits
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                         for (int t = 0; t < 8; ++t) {
                             const uint32_t job = (t & 1) ? (w4[t >> 1] >> 16) : (w4[t >> 1] & 0xffffu);
                             if (sg * 256 + lane * 8 + t < dL && job < (uint32_t)n)
-                                Uw[(job * W + warp) * NPL + q] &= clr;
+                                Uw[job * urow + warp * NPL + q] &= clr;
                         }
                     }
                     __syncwarp();
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                     const uint32_t clr = ~(1u << L);
                     for (int i = lane; i < dL; i += 32) {
                         const uint32_t job = row[i];
-                        if (job < (uint32_t)n) Uw[(job * W + warp) * NPL + q] &= clr;
+                        if (job < (uint32_t)n) Uw[job * urow + warp * NPL + q] &= clr;
                     }
                     __syncwarp();
                 }
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                 uint32_t any = 0;
                 if (j < n) {
 #pragma unroll
-                    for (int q = 0; q < NPL; ++q) any |= Uw[(j * W + warp) * NPL + q];
+                    for (int q = 0; q < NPL; ++q) any |= Uw[j * urow + warp * NPL + q];
                 }
                 const uint32_t bal = __ballot_sync(0xffffffffu, any != 0);
                 if (lane == (j0 >> 5)) livew = bal;
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
             }
             int cnt = 0;
             for (int j = 0; j < n; ++j) {
-                const uint32_t uj = Uw[(j * W + warp) * NPL + q];
+                const uint32_t uj = Uw[j * urow + warp * NPL + q];
                 if (uj == 0) continue; // scheduled in every node of this half-warp
                 if (uj & lanebit) {
                     ++cnt;
@@ -726,9 +727,14 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
             // int32 walk ORs the warp offset into the record address: 4*npl*W
             // must be a power of two (s16 adds it on the FMA pipe instead)
             if (!pl.s16 && ((4 * npl * W) & (4 * npl * W - 1))) continue;
-            if (pl.smem_base + (size_t)(n + 1) * 4 * npl * W > 65536) continue; // 16-bit U addresses
+            // sparse-plan rows are padded by npl words so the per-job rows of
+            // one warp spread over the banks (building U touches 32 different
+            // jobs at once; it dominates for deep B&B nodes, not for D1 pools)
+            const int urow = npl * W + (pl.sparse ? npl : 0);
+            if (pl.smem_base + (size_t)(n + 1) * 4 * urow > 65536) continue; // 16-bit U addresses
             fsp_lb_layout L{};
-            L.u_bytes = align16((size_t)(n + 1) * 4 * npl * W);
+            L.urow_words = urow;
+            L.u_bytes = align16((size_t)(n + 1) * 4 * urow);
             L.off_u = 0;
             L.ptm_bytes = align16((size_t)n * mp4 * 4);
             L.off_ptm = L.u_bytes;
