@@ -730,7 +730,9 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
             // sparse-plan rows are padded by npl words so the per-job rows of
             // one warp spread over the banks (building U touches 32 different
             // jobs at once; it dominates for deep B&B nodes, not for D1 pools)
-            const int urow = npl * W + (pl.sparse ? npl : 0);
+            bool pad = pl.sparse;
+            if (const char *e = getenv("FSP_LB_PAD")) pad = atoi(e) != 0 && pl.s16;
+            const int urow = npl * W + (pad ? npl : 0);
             if (pl.smem_base + (size_t)(n + 1) * 4 * urow > 65536) continue; // 16-bit U addresses
             fsp_lb_layout L{};
             L.urow_words = urow;
