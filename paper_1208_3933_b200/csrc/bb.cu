@@ -64,6 +64,8 @@ struct BBState {
     int64_t *off;         // exclusive scan of plan; off[B] = (kept << 32) | children
     int64_t *d_count;     // children this iteration (LB pool size)
     int64_t *boff;        // survivor offsets per prune block
+    long long *tsum;      // device_scan scratch: tile sums and their offsets
+    int64_t *toff;
     int32_t *bcnt;
     int32_t *d_inc;       // incumbent makespan (pruning threshold)
     unsigned long long *d_cand;
@@ -116,8 +118,10 @@ __device__ __forceinline__ long long block_excl_scan(long long v, long long &tot
     return r;
 }
 
-// Exclusive scan of N items (single block); out[N] = total.  Items are int64
-// (in64) or int32 (in32).  If count_out: *count_out = low 32 bits of the total.
+// Exclusive scan of N items; out[N] = total.  Items are int64 (in64) or int32
+// (in32).  If count_out: *count_out = low 32 bits of the total.
+// Large N: scan_local_kernel scans 1024-item tiles in parallel and writes tile
+// sums, scan_kernel (one block) scans the sums, scan_add_kernel adds them back.
 __global__ void __launch_bounds__(kScanThreads)
     scan_kernel(const long long *in64, const int32_t *in32, int64_t N, int64_t *out,
                 int64_t *count_out)
@@ -136,6 +140,33 @@ __global__ void __launch_bounds__(kScanThreads)
         out[N] = carry;
         if (count_out) *count_out = carry & 0xffffffffll;
     }
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    scan_local_kernel(const long long *in64, const int32_t *in32, int64_t N, int64_t *out,
+                      long long *tile_sums)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    long long v = 0;
+    if (i < N) v = in64 ? in64[i] : (long long)in32[i];
+    long long tot;
+    const long long ex = block_excl_scan(v, tot);
+    if (i < N) out[i] = ex;
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    scan_add_kernel(int64_t N, int64_t *out, const int64_t *tile_off)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < N) out[i] += tile_off[blockIdx.x];
+}
+
+__global__ void scan_total_kernel(int64_t N, int64_t *out, const int64_t *tile_off, int64_t tiles,
+                                  int64_t *count_out)
+{
+    out[N] = tile_off[tiles];
+    if (count_out) *count_out = tile_off[tiles] & 0xffffffffll;
 }
 
 // Selection (a9) bookkeeping: per popped parent, children to generate now
@@ -164,9 +195,12 @@ __global__ void plan_kernel(Nodes st, int64_t first, int64_t B, int n, int K, co
 }
 
 // Branching (a7): one warp per parent; its unscheduled jobs of ascending rank
-// cur .. cur+g-1 become children prefix + j with C'_0 = C_0 + p_j0,
-// C'_k = max(C'_k-1, C_k) + p_jk; a parent with children left is
-// copied to the kept buffer with its cursor advanced.
+// cur .. cur+g-1 become children prefix + j; lane t < g owns child
+// t.  Child completion times C'_0 = C_0 + p_j0, C'_k = max(C'_k-1, C_k) + p_jk
+// are one max-plus scan across lanes = machines:
+//   C'_k = S_k + max_{i<=k} (C_i - S_i-1),  S_k = sum_{i<=k} p_ji.
+// A parent with children left is copied to the kept buffer, cursor advanced.
+// Rows are 16-byte aligned (stride is a multiple of 8): copies move uint4s.
 __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t *__restrict__ off,
                               Nodes ch, Nodes kp, const int32_t *__restrict__ ptm, int n, int m,
                               int stride)
@@ -175,49 +209,83 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int nw = (n + 31) >> 5;
     uint32_t *bm = bm_all + wib * nw;
+    const int s8 = stride >> 3; // uint4 per row
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; p < B; p += warps) {
         const int64_t src = first + p;
-        const uint16_t *row = st.pf + (size_t)src * stride;
+        const uint4 *row4 = reinterpret_cast<const uint4 *>(st.pf + (size_t)src * stride);
         const int d = st.dp[src], cur = st.cur[src];
         const long long o0 = off[p], o1 = off[p + 1];
         const int g = (int)((o1 & 0xffffffffll) - (o0 & 0xffffffffll));
         const int keep = (int)((o1 >> 32) - (o0 >> 32));
-        int64_t c = o0 & 0xffffffffll;
+        const int64_t c0 = o0 & 0xffffffffll;
+        const int d8 = (d + 7) >> 3; // uint4 holding prefix entries
         if (g > 0) {
+            // scheduled-job bitmap from the prefix, eight ids per load
             for (int w = lane; w < nw; w += 32) bm[w] = 0;
             __syncwarp();
-            for (int i = lane; i < d; i += 32) atomicOr(&bm[row[i] >> 5], 1u << (row[i] & 31));
-            __syncwarp();
-            int rank = 0;
-            for (int w = 0; w < nw && rank < cur + g; ++w) {
-                uint32_t freeb = ~bm[w];
-                if (w == nw - 1 && (n & 31)) freeb &= (1u << (n & 31)) - 1;
-                while (freeb && rank < cur + g) {
-                    const int j = w * 32 + __ffs(freeb) - 1;
-                    freeb &= freeb - 1;
-                    if (rank++ < cur) continue;
-                    uint16_t *crow = ch.pf + (size_t)c * stride;
-                    for (int i = lane; i < d; i += 32) crow[i] = row[i];
-                    if (lane == 0) {
-                        crow[d] = (uint16_t)j;
-                        ch.dp[c] = d + 1;
-                        const int32_t *pc = st.C + (size_t)src * m;
-                        int32_t *cc = ch.C + (size_t)c * m;
-                        int prev = 0;
-                        for (int k = 0; k < m; ++k) {
-                            prev = max(prev, pc[k]) + ptm[j * m + k];
-                            cc[k] = prev;
-                        }
-                    }
-                    ++c;
+            for (int q = lane; q < d8; q += 32) {
+                const uint4 v = row4[q];
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const uint32_t j = (t & 1) ? (w4[t >> 1] >> 16) : (w4[t >> 1] & 0xffffu);
+                    if (q * 8 + t < d) atomicOr(&bm[j >> 5], 1u << (j & 31));
                 }
+            }
+            __syncwarp();
+            // lane t < g: the unscheduled job of rank cur + t
+            int myj = -1;
+            {
+                const int r = cur + lane;
+                int base = 0;
+                for (int w = 0; w < nw; ++w) {
+                    uint32_t freeb = ~bm[w];
+                    if (w == nw - 1 && (n & 31)) freeb &= (1u << (n & 31)) - 1;
+                    const int c = __popc(freeb);
+                    if (lane < g && myj < 0 && r < base + c) myj = w * 32 + (__fns(freeb, 0, r - base + 1));
+                    base += c;
+                }
+            }
+            // prefixes: every child row = the parent's row with its job at d
+            for (int t = 0; t < g; ++t) {
+                const int j = __shfl_sync(0xffffffffu, myj, t);
+                uint4 *crow4 = reinterpret_cast<uint4 *>(ch.pf + (size_t)(c0 + t) * stride);
+                for (int q = lane; q <= (d >> 3) && q < s8; q += 32) {
+                    uint4 v = q < d8 ? row4[q] : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu,
+                                                           0xffffffffu);
+                    if (q == (d >> 3)) { // insert j at position d
+                        uint32_t *w4 = reinterpret_cast<uint32_t *>(&v);
+                        const int t8 = d & 7;
+                        uint32_t &wd = w4[t8 >> 1];
+                        wd = (t8 & 1) ? ((wd & 0xffffu) | ((uint32_t)j << 16))
+                                      : ((wd & 0xffff0000u) | (uint32_t)j);
+                    }
+                    crow4[q] = v;
+                }
+                // completion times: one max-plus scan over machines (lanes)
+                const int pk = lane < m ? ptm[j * m + lane] : 0;
+                const int ck = lane < m ? st.C[(size_t)src * m + lane] : 0;
+                int S = pk;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, S, o);
+                    if (lane >= o) S += y;
+                }
+                int M = ck - (S - pk);
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, M, o);
+                    if (lane >= o) M = max(M, y);
+                }
+                if (lane < m) ch.C[(size_t)(c0 + t) * m + lane] = S + M;
+                if (lane == 0) ch.dp[c0 + t] = d + 1;
             }
         }
         if (keep) {
             const int64_t dst = o0 >> 32;
-            uint16_t *krow = kp.pf + (size_t)dst * stride;
-            for (int i = lane; i < d; i += 32) krow[i] = row[i];
+            uint4 *krow4 = reinterpret_cast<uint4 *>(kp.pf + (size_t)dst * stride);
+            for (int q = lane; q < d8; q += 32) krow4[q] = row4[q];
             for (int k = lane; k < m; k += 32) kp.C[(size_t)dst * m + k] = st.C[(size_t)src * m + k];
             if (lane == 0) {
                 kp.dp[dst] = d;
@@ -240,8 +308,9 @@ __global__ void restore_kernel(Nodes kp, const int64_t *off_B, int64_t first, No
          q += warps) {
         const int d = kp.dp[q];
         const int64_t dst = first + q;
-        for (int i = lane; i < d; i += 32)
-            st.pf[(size_t)dst * stride + i] = kp.pf[(size_t)q * stride + i];
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(kp.pf + (size_t)q * stride);
+        uint4 *d4 = reinterpret_cast<uint4 *>(st.pf + (size_t)dst * stride);
+        for (int i = lane; i < ((d + 7) >> 3); i += 32) d4[i] = s4[i];
         for (int k = lane; k < m; k += 32) st.C[(size_t)dst * m + k] = kp.C[(size_t)q * m + k];
         if (lane == 0) {
             st.dp[dst] = d;
@@ -391,6 +460,8 @@ void bb_free(BBState *s)
     cudaFree(s->d_count);
     cudaFree(s->boff);
     cudaFree(s->bcnt);
+    cudaFree(s->tsum);
+    cudaFree(s->toff);
     cudaFree(s->d_inc);
     cudaFree(s->d_cand);
     cudaFree(s->d_packed);
@@ -496,6 +567,21 @@ int push_host(BBState *s, const std::vector<uint16_t> &pf, const std::vector<int
     return FSP_OK;
 }
 
+void device_scan(BBState *s, const long long *in64, const int32_t *in32, int64_t N, int64_t *out,
+                 int64_t *count_out)
+{
+    cudaStream_t st = s->stream;
+    if (N <= 4 * kScanThreads) {
+        scan_kernel<<<1, kScanThreads, 0, st>>>(in64, in32, N, out, count_out);
+        return;
+    }
+    const int64_t tiles = (N + kScanThreads - 1) / kScanThreads;
+    scan_local_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(in64, in32, N, out, s->tsum);
+    scan_kernel<<<1, kScanThreads, 0, st>>>(s->tsum, nullptr, tiles, s->toff, nullptr);
+    scan_add_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(N, out, s->toff);
+    scan_total_kernel<<<1, 1, 0, st>>>(N, out, s->toff, tiles, count_out);
+}
+
 // One select / branch / bound / eliminate iteration.
 int bb_iterate(BBState *s)
 {
@@ -517,7 +603,7 @@ int bb_iterate(BBState *s)
     const int pb = 256;
     plan_kernel<<<(unsigned)((B + pb - 1) / pb), pb, 0, st>>>(s->st, first, B, n, K, s->d_inc,
                                                               s->plan, s->d_stats);
-    scan_kernel<<<1, kScanThreads, 0, st>>>(s->plan, nullptr, B, s->off, s->d_count);
+    device_scan(s, s->plan, nullptr, B, s->off, s->d_count);
     const int ewarps = 8;
     const int eblocks = (int)std::min<int64_t>((B + ewarps - 1) / ewarps, 148 * 16);
     expand_kernel<<<eblocks, ewarps * 32, ewarps * ((n + 31) / 32) * 4, st>>>(
@@ -532,7 +618,7 @@ int bb_iterate(BBState *s)
     const int nblk = (int)((maxC + kPruneThreads - 1) / kPruneThreads);
     prune_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->d_count, n, s->d_inc, s->d_cand, s->bcnt,
                                                   s->d_stats);
-    scan_kernel<<<1, kScanThreads, 0, st>>>(nullptr, s->bcnt, nblk, s->boff, nullptr);
+    device_scan(s, nullptr, s->bcnt, nblk, s->boff, nullptr);
     scatter_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->d_count, off_B, n, m, stride, s->d_inc,
                                                     s->boff, first, s->st);
     commit_kernel<<<1, 256, 0, st>>>(s->ch, n, stride, s->d_inc, s->d_cand, s->d_perm, s->d_packed,
@@ -600,6 +686,8 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     alloc((void **)&s->d_count, 8);
     alloc((void **)&s->boff, (size_t)(nblk + 1) * 8);
     alloc((void **)&s->bcnt, (size_t)nblk * 4);
+    alloc((void **)&s->tsum, (size_t)(s->kcap / kScanThreads + 2) * 8);
+    alloc((void **)&s->toff, (size_t)(s->kcap / kScanThreads + 3) * 8);
     alloc((void **)&s->d_inc, 4);
     alloc((void **)&s->d_cand, 8);
     alloc((void **)&s->d_packed, 8);

@@ -1,2 +1,2 @@
-for w in 14 12 8; do FSP_LB_PAD=1 FSP_LB_NPL=4 SWEEP_WARPS=$w timeout 600 python tools/lb_sweep.py ta091:1048576 2>&1 | tail -1; done
-FSP_LB_PAD=1 timeout 600 python tools/lb_sweep.py ta091:1048576 2>&1 | tail -1
+timeout 600 python tools/bb_try.py ta091:2147483647:15 ta051:2147483647:10 ta021:2147483647:10 ta002:2147483647:10 > gpurun_out/bbt.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_bb.py tests/test_gpu_parity.py -x -q 2>&1 | tail -2 >> gpurun_out/bbt.txt
