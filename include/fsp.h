@@ -71,6 +71,8 @@ typedef struct {
     int32_t smem_bytes;       /* dynamic shared memory per CTA             */
     int32_t maxm;             /* machine-count specialisation used         */
     int64_t table_bytes;      /* device bytes of the couple tables         */
+    int32_t nodes_per_lane;   /* sub-problems per thread in the lb kernel  */
+    int32_t walk16;           /* 1: 16-bit walk (values fit int16)         */
 } fsp_instance_info;
 
 int fsp_instance_get_info(const fsp_instance *inst, fsp_instance_info *info);

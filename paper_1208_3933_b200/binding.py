@@ -41,7 +41,8 @@ class InstanceInfo(C.Structure):
     _fields_ = [("n", C.c_int32), ("m", C.c_int32), ("P", C.c_int32), ("device", C.c_int32),
                 ("groups", C.c_int32), ("pairs_per_group", C.c_int32),
                 ("warps_per_cta", C.c_int32), ("ctas_per_sm", C.c_int32),
-                ("smem_bytes", C.c_int32), ("maxm", C.c_int32), ("table_bytes", C.c_int64)]
+                ("smem_bytes", C.c_int32), ("maxm", C.c_int32), ("table_bytes", C.c_int64),
+                ("nodes_per_lane", C.c_int32), ("walk16", C.c_int32)]
 
 
 class BBStats(C.Structure):

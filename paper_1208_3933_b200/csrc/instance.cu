@@ -185,5 +185,7 @@ extern "C" int fsp_instance_get_info(const fsp_instance *inst, fsp_instance_info
     info->smem_bytes = (int32_t)pl.smem_bytes;
     info->maxm = pl.maxm;
     info->table_bytes = inst->table_bytes;
+    info->nodes_per_lane = pl.npl;
+    info->walk16 = pl.s16 ? 1 : 0;
     return FSP_OK;
 }

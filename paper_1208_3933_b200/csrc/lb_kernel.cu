@@ -121,6 +121,29 @@ __device__ __forceinline__ uint32_t mask_addr(uint32_t meta, uint32_t wst, uint3
     else return (meta & 0xffffu) | wst;
 }
 
+// U row layouts (one row per job, one segment per warp):
+//  * lane-major (int32 walk): NPL words, bit L of word q = node q*32+L;
+//  * nibble (s16 walk): lane L owns NPL+1 consecutive bits of word L/LPW at
+//    shift (L % LPW)*(NPL+1); bit 1+q = node q*32+L (bit 0 stays clear).  A
+//    lane loads one word, shifts once, and R2P turns its NPL bits into the
+//    predicates P1..P4 of the updates (instead of one LOP3 per node: the ALU
+//    pipe is the walk's bottleneck).
+template <int NPL>
+struct Nib {
+    static constexpr int LPW = 32 / (NPL + 1);         // lanes per word
+    static constexpr int WPR = (32 + LPW - 1) / LPW;   // words per warp segment
+};
+
+template <bool S16, int NPL, int MAXM>
+struct ULayout {
+    // nibble rows where the couple walk dominates (m >= 10); lane-major rows for
+    // m = 5, where the per-node phase dominates (measured on 20x5)
+    static constexpr bool NIB = S16 && MAXM >= 10;
+    static constexpr int WPR = NIB ? Nib<NPL>::WPR : NPL;
+    __device__ static int word(int L, int q) { return NIB ? L / Nib<NPL>::LPW : q; }
+    __device__ static int bit(int L, int q) { return NIB ? (L % Nib<NPL>::LPW) * (NPL + 1) + 1 + q : L; }
+};
+
 // The NPL unscheduled-bit words of one job for this warp's NPL*32 nodes.
 template <int NPL>
 struct Mask {
@@ -131,10 +154,12 @@ template <int NPL>
 __device__ __forceinline__ Mask<NPL> lds_mask(uint32_t addr)
 {
     Mask<NPL> v;
-    if constexpr (NPL == 2) {
+    if constexpr (NPL == 1) {
+        asm("ld.shared.u32 %0, [%1];" : "=r"(v.b[0]) : "r"(addr));
+    } else if constexpr (NPL == 2) {
         asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.b[0]), "=r"(v.b[1]) : "r"(addr));
     } else {
-        static_assert(NPL == 4, "NPL is 2 or 4");
+        static_assert(NPL == 4, "NPL is 1, 2 or 4");
         asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
             : "=r"(v.b[0]), "=r"(v.b[1]), "=r"(v.b[2]), "=r"(v.b[3])
             : "r"(addr));
@@ -164,11 +189,18 @@ __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1
     }
 }
 
-#define FSP_MASK(META) lds_mask<NPL>(mask_addr<S16>((META), wst, hi_mul, wst64))
+// nibble layout: one word per lane (MW = 1); lane-major: NPL words
+#define FSP_MASK(META) lds_mask<MW>(mask_addr<S16>((META), wst, hi_mul, wst64))
 #define FSP_UPD(MASK, C1, META)                                                 \
     {                                                                           \
-        _Pragma("unroll") for (int q_ = 0; q_ < NPL; ++q_)                      \
-            upd<S16>((MASK).b[q_], lanebit, (C1), (META), uu[q_], ww[q_]);      \
+        if constexpr (UL::NIB) {                                                \
+            const uint32_t nb_ = (MASK).b[0] >> lsh;                            \
+            _Pragma("unroll") for (int q_ = 0; q_ < NPL; ++q_)                  \
+                upd<S16>(nb_, 2u << q_, (C1), (META), uu[q_], ww[q_]);          \
+        } else {                                                                \
+            _Pragma("unroll") for (int q_ = 0; q_ < NPL; ++q_)                  \
+                upd<S16>((MASK).b[q_], lanebit, (C1), (META), uu[q_], ww[q_]);  \
+        }                                                                       \
     }
 
 template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE>
@@ -226,10 +258,16 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     const long long ntiles = (pool + TN - 1) / TN;
     const long long nchunks = (ntiles + W - 1) / W;
     const uint32_t lanebit = 1u << lane;
-    const uint32_t wst = 4u * NPL * warp;
+    using UL = ULayout<S16, NPL, MAXM>;
+    constexpr int WPR = UL::WPR;                 // U words per warp per job row
+    constexpr int MW = UL::NIB ? 1 : NPL;        // mask words a lane loads
+    const int lw = UL::word(lane, 0);            // nibble layout: this lane's word
+    const int lsh = UL::NIB ? UL::bit(lane, 0) - 1 : 0; // ... and bit offset
+    const uint32_t wst = 4u * (WPR * warp + (UL::NIB ? lw : 0));
     const int urow = a.L.urow_words; // words per job row of U (padded against bank conflicts)
     const uint32_t hi_mul = a.hi_mul;
     const uint64_t wst64 = (uint64_t)wst << 32;
+    const int useg = WPR * warp; // this warp's segment of a U row
 
     for (long long chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
         const long long tile = chunk * W + warp;
@@ -253,10 +291,23 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
             validq[q] = __ballot_sync(0xffffffffu, has);
             anyvalid |= validq[q];
         }
+        // all-unscheduled pattern of this warp's segment
+        uint32_t pat[WPR];
+        if constexpr (UL::NIB) {
+            uint32_t mine = 0;
+#pragma unroll
+            for (int q = 0; q < NPL; ++q)
+                if ((validq[q] >> lane) & 1u) mine |= 1u << UL::bit(lane, q);
+#pragma unroll
+            for (int w = 0; w < WPR; ++w) pat[w] = __reduce_or_sync(0xffffffffu, lw == w ? mine : 0u);
+        } else {
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) pat[q] = validq[q];
+        }
         for (int j = lane; j <= n; j += 32) {
 #pragma unroll
-            for (int q = 0; q < NPL; ++q) // row n: the padding record's always-empty mask
-                Uw[j * urow + warp * NPL + q] = j < n ? validq[q] : 0u;
+            for (int w = 0; w < WPR; ++w) // row n: the padding record's always-empty mask
+                Uw[j * urow + useg + w] = j < n ? pat[w] : 0u;
         }
         __syncwarp();
         // coalesced pass over the TN prefix records: clear the scheduled bits
@@ -280,7 +331,8 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                 uint4 cur = load_row(0, 0);
                 for (int L = 0; L < 32; ++L) {
                     const int dL = __shfl_sync(0xffffffffu, dq[q], L);
-                    const uint32_t clr = ~(1u << L);
+                    const uint32_t clr = ~(1u << UL::bit(L, q));
+                    const int uwd = useg + UL::word(L, q);
                     const uint4 nxt = L + 1 < 32 ? load_row(L + 1, 0) : cur;
                     for (int sg = 0; sg * 256 < dL; ++sg) {
                         if (sg > 0) cur = load_row(L, sg);
@@ -289,7 +341,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                         for (int t = 0; t < 8; ++t) {
                             const uint32_t job = (t & 1) ? (w4[t >> 1] >> 16) : (w4[t >> 1] & 0xffffu);
                             if (sg * 256 + lane * 8 + t < dL && job < (uint32_t)n)
-                                Uw[job * urow + warp * NPL + q] &= clr;
+                                Uw[job * urow + uwd] &= clr;
                         }
                     }
                     __syncwarp();
@@ -300,10 +352,11 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                     const int dL = __shfl_sync(0xffffffffu, dq[q], L);
                     if (dL == 0) continue;
                     const uint16_t *row = a.prefix + (size_t)(tile * TN + q * 32 + L) * a.stride;
-                    const uint32_t clr = ~(1u << L);
+                    const uint32_t clr = ~(1u << UL::bit(L, q));
+                    const int uwd = useg + UL::word(L, q);
                     for (int i = lane; i < dL; i += 32) {
                         const uint32_t job = row[i];
-                        if (job < (uint32_t)n) Uw[job * urow + warp * NPL + q] &= clr;
+                        if (job < (uint32_t)n) Uw[job * urow + uwd] &= clr;
                     }
                     __syncwarp();
                 }
@@ -321,7 +374,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                 uint32_t any = 0;
                 if (j < n) {
 #pragma unroll
-                    for (int q = 0; q < NPL; ++q) any |= Uw[j * urow + warp * NPL + q];
+                    for (int w = 0; w < WPR; ++w) any |= Uw[j * urow + useg + w];
                 }
                 const uint32_t bal = __ballot_sync(0xffffffffu, any != 0);
                 if (lane == (j0 >> 5)) livew = bal;
@@ -403,9 +456,14 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
             }
             int cnt = 0;
             for (int j = 0; j < n; ++j) {
-                const uint32_t uj = Uw[j * urow + warp * NPL + q];
-                if (uj == 0) continue; // scheduled in every node of this half-warp
-                if (uj & lanebit) {
+                const uint32_t uj = Uw[j * urow + useg + UL::word(lane, q)];
+                const bool act = (uj >> UL::bit(lane, q)) & 1u;
+                if constexpr (UL::NIB) {
+                    if (!__any_sync(0xffffffffu, act)) continue; // scheduled everywhere
+                } else {
+                    if (uj == 0) continue; // scheduled in every node of this half-warp
+                }
+                if (act) {
                     ++cnt;
                     const int4 *pr = reinterpret_cast<const int4 *>(s_ptm + j * a.mp4);
                     int p[MAXM];
@@ -541,12 +599,12 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                 // X/Y register sets alternate so no copies are needed.
                 uint4 xa = rp[0], xb = rp[1]; // step 0
                 uint4 ya = rp[2], yb = rp[3]; // step 1
-                Mask<NPL> mx0 = FSP_MASK(xa.y), mx1 = FSP_MASK(xa.w);
-                Mask<NPL> mx2 = FSP_MASK(xb.y), mx3 = FSP_MASK(xb.w);
+                Mask<MW> mx0 = FSP_MASK(xa.y), mx1 = FSP_MASK(xa.w);
+                Mask<MW> mx2 = FSP_MASK(xb.y), mx3 = FSP_MASK(xb.w);
                 int s = 0;
                 for (; s + 2 <= n4c; s += 2) {
-                    const Mask<NPL> my0 = FSP_MASK(ya.y), my1 = FSP_MASK(ya.w);
-                    const Mask<NPL> my2 = FSP_MASK(yb.y), my3 = FSP_MASK(yb.w);
+                    const Mask<MW> my0 = FSP_MASK(ya.y), my1 = FSP_MASK(ya.w);
+                    const Mask<MW> my2 = FSP_MASK(yb.y), my3 = FSP_MASK(yb.w);
                     FSP_UPD(mx0, xa.x, xa.y);
                     FSP_UPD(mx1, xa.z, xa.w);
                     FSP_UPD(mx2, xb.x, xb.y);
@@ -711,8 +769,8 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     pl.npl = 2;
     // Candidates: nodes per lane (4 only for the exact-m specialisations), warps
     // per CTA, fewest couple groups that fit.  Score = resident warps per SM
-    // (latency hiding) x 1.3 for 4 nodes per lane (half the table and mask
-    // traffic per node; +10 % measured at 200x20) / (1 + 1.5 % per extra group
+    // (latency hiding) x 1.5 for 4 nodes per lane (half the table and mask
+    // traffic per node; +18 % measured at 200x20) / (1 + 1.5 % per extra group
     // reload).  Env FSP_LB_NPL / FSP_LB_WARPS pin a choice (sweeps, tests).
     int npl_lo = 2, npl_hi = pl.exact ? 4 : 2;
     if (const char *s = getenv("FSP_LB_NPL")) npl_lo = npl_hi = (atoi(s) == 4 && pl.exact) ? 4 : 2;
@@ -724,15 +782,21 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     fsp_lb_plan bestp = pl;
     for (int npl = npl_lo; npl <= npl_hi; npl += 2) {
         for (int W = w_hi; W >= w_lo; --W) {
+            // warps are dealt to the 4 SMSPs by id % 4: a W that is not a multiple
+            // of 4 leaves some SMSPs with an extra warp that paces the whole CTA
+            // (measured: 200x20, 10 warps 120 M/s vs 12 warps 140 M/s)
+            if (W % 4 != 0 && w_lo != w_hi) continue;
             // int32 walk ORs the warp offset into the record address: 4*npl*W
             // must be a power of two (s16 adds it on the FMA pipe instead)
             if (!pl.s16 && ((4 * npl * W) & (4 * npl * W - 1))) continue;
             // sparse-plan rows are padded by npl words so the per-job rows of
             // one warp spread over the banks (building U touches 32 different
             // jobs at once; it dominates for deep B&B nodes, not for D1 pools)
-            bool pad = pl.sparse;
-            if (const char *e = getenv("FSP_LB_PAD")) pad = atoi(e) != 0 && pl.s16;
-            const int urow = npl * W + (pad ? npl : 0);
+            // s16: nibble rows (one word per lane, ceil(32/LPW) words per warp);
+            // made odd so the 32 jobs a warp clears at once hit 32 banks
+            const bool nib = pl.s16 && pl.maxm >= 10; // = ULayout::NIB
+            const int lpw = 32 / (npl + 1), wpr = nib ? (32 + lpw - 1) / lpw : npl;
+            const int urow = nib ? (wpr * W) | 1 : npl * W;
             if (pl.smem_base + (size_t)(n + 1) * 4 * urow > 65536) continue; // 16-bit U addresses
             fsp_lb_layout L{};
             L.urow_words = urow;
@@ -763,7 +827,7 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                     c.warps = W;
                     c.smem_bytes = L.off_tab + gb;
                     if (occupancy_of(c) == FSP_OK && c.ctas_per_sm > 0) {
-                        const double score = (double)W * c.ctas_per_sm * (npl == 4 ? 1.3 : 1.0) /
+                        const double score = (double)W * c.ctas_per_sm * (npl == 4 ? 1.5 : 1.0) /
                                              (1.0 + 0.015 * (Greal - 1));
                         if (score > best) {
                             best = score;

@@ -36,7 +36,8 @@ def time_cfg(name, N, warps=None, reps=5):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     info = inst.info
-    return {"cfg": name, "N": N, "warps": info["warps_per_cta"], "groups": info["groups"],
+    return {"cfg": name, "N": N, "npl": info["nodes_per_lane"], "warps": info["warps_per_cta"],
+            "groups": info["groups"],
             "ctas_per_sm": info["ctas_per_sm"], "smem": info["smem_bytes"], "ms": round(ms, 3),
             "Mbounds_s": round(N / ms / 1e3, 2)}
 
@@ -48,6 +49,11 @@ if __name__ == "__main__":
         for npl in os.environ.get("SWEEP_NPL", "0").split(","):
             os.environ["FSP_LB_NPL"] = npl
             for w in ([int(x) for x in os.environ.get("SWEEP_WARPS", "0").split(",")]):
-                r = time_cfg(name, int(N), w)
+                try:
+                    r = time_cfg(name, int(N), w)
+                except Exception as ex:  # a shape that does not fit: skip
+                    print(json.dumps({"cfg": name, "npl_env": int(npl), "warps_env": w,
+                                      "error": str(ex)[:120]}), flush=True)
+                    continue
                 r["npl_env"] = int(npl)
                 print(json.dumps(r), flush=True)
