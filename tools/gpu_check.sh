@@ -1,3 +1,3 @@
-SWEEP_NPL=0 SWEEP_WARPS=0 timeout 600 python tools/lb_sweep.py ta091:1048576 ta051:1048576 ta021:1048576 ta001:1048576 ta111:262144 2>&1 | grep cfg > gpurun_out/sweep_grid.txt
-timeout 600 python tools/bb_try.py ta091:2147483647:15 ta051:2147483647:10 ta021:2147483647:10 >> gpurun_out/sweep_grid.txt 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_bb.py -x -q 2>&1 | tail -2 >> gpurun_out/sweep_grid.txt
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:lb_kernel -s 3 -c 1 -o gpurun_out/prof_lb6 python bench.py --steps 1 --warmup 3 --no-bb --no-e2e --cpu-seconds 1 > gpurun_out/ncu6.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 5 --warmup 3 --no-bb --no-e2e --cpu-seconds 1 > gpurun_out/ncu_launch_bench.log 2>&1
