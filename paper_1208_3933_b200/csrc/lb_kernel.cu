@@ -103,6 +103,7 @@ struct LbArgs {
     uint32_t hi_mul;       // 0x10000 (see mask_addr)
     const int32_t *cin;    // optional prefix completion times [pool][cin_stride]
     int cin_stride;
+    int vec_rows;          // vectorised scheduled-set build (long prefixes)
 };
 
 // Shared address of U[job][warp] from a record's meta word (wst = 4*NPL*warp).
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
         // coalesced pass over the TN prefix records: clear the scheduled bits
         // (16-byte rows: each lane takes eight job ids per vector load; the
         // next node's row is loaded while this one's bits are cleared)
-        const bool rows16 = ((reinterpret_cast<uintptr_t>(a.prefix) | ((uintptr_t)a.stride * 2)) & 15) == 0;
+        const bool rows16 = a.vec_rows && ((reinterpret_cast<uintptr_t>(a.prefix) | ((uintptr_t)a.stride * 2)) & 15) == 0;
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
             if (rows16) {
@@ -865,6 +866,9 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.ptm = inst->d_ptm32s;
     a.cin = cin;
     a.cin_stride = cin_stride;
+    // eight job ids per lane pay off only for long prefixes (measured: 20x5 and
+    // 20x20 faster with one id per lane, 200x20 faster with eight)
+    a.vec_rows = getenv("FSP_LB_VECROWS") ? atoi(getenv("FSP_LB_VECROWS")) : (inst->n >= 128);
     a.prefix = prefix;
     a.depth = depth;
     a.lb_out = lb_out;
