@@ -241,9 +241,21 @@ def main():
     rank, world, local = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device")
+    # one process per GPU over NCCL; FSP_BENCH_BACKEND=gloo runs the same
+    # multi-rank control flow with host-side collectives (testing on one GPU)
+    backend = os.environ.get("FSP_BENCH_BACKEND", "nccl")
+    comm = "cuda" if backend == "nccl" else "cpu"
+    ndev = torch.cuda.device_count()
+    if world > ndev and "FSP_BB_MEM_FRAC" not in os.environ:
+        # ranks sharing a device split the B&B stack budget between them
+        os.environ["FSP_BB_MEM_FRAC"] = str(0.4 / -(-world // ndev))
+    local = local % ndev
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg = a.config
     n, m, seed = inputs.TAILLARD_SEEDS[cfg]
     ptm = inputs.taillard(n, m, seed)
@@ -277,7 +289,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
     ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms], dtype=torch.float64, device=comm)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -302,7 +314,7 @@ def main():
             inst.lb_eval_host_ptr(h_pf.data_ptr(), stride, h_dp.data_ptr(), a.pool,
                                   h_lb.data_ptr())
         dt = time.perf_counter() - t0
-        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([dt], dtype=torch.float64, device=comm)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
@@ -325,9 +337,9 @@ def main():
                       "status": int(rc), "incumbent": msp, **st}
             else:
                 state = binding.BBState(inst, 2**31 - 1, rank, world)
-                eng = fdist.DeviceEngine(state, "cuda")
+                eng = fdist.DeviceEngine(state, "cuda", comm)
                 barrier()
-                res = fdist.distributed_bb(eng, dist, rank=rank, world=world, device="cuda",
+                res = fdist.distributed_bb(eng, dist, rank=rank, world=world, device=comm,
                                            sync_every=8, time_limit_s=a.bb_seconds)
                 bb = {"bounded_nodes_per_s": res.bounded / max(res.wall_s, 1e-9),
                       "status": res.status, "incumbent": res.makespan, "bounded": res.bounded,

@@ -166,13 +166,15 @@ def distributed_bb(engine, dist, group=None, *, rank: int, world: int, device="c
 
 
 class DeviceEngine:
-    """Adapter: binding.BBState on this rank's GPU, node buffers as CUDA uint8
-    tensors (NCCL point-to-point over NVLink)."""
+    """Adapter: binding.BBState on this rank's GPU.  Node buffers are CUDA
+    uint8 tensors (NCCL point-to-point over NVLink); with comm_device="cpu"
+    (gloo) they are staged through host memory."""
 
-    def __init__(self, state, device):
+    def __init__(self, state, device, comm_device=None):
         self.state = state
         self.n = state.n
         self.device = device
+        self.comm = comm_device or device
         self.node_bytes = state.node_bytes()
 
     def step(self, iters):
@@ -195,12 +197,16 @@ class DeviceEngine:
 
     def alloc_node_buffer(self, k):
         import torch
-        return torch.empty(k * self.node_bytes, dtype=torch.uint8, device=self.device)
+        return torch.empty(k * self.node_bytes, dtype=torch.uint8, device=self.comm)
 
     def export_nodes(self, k):
-        buf = self.alloc_node_buffer(k)
+        import torch
+        buf = torch.empty(k * self.node_bytes, dtype=torch.uint8, device=self.device)
         got = self.state.export(k, buf.data_ptr())
-        return buf[:got * self.node_bytes], got
+        out = buf[:got * self.node_bytes]
+        return (out if self.comm == self.device else out.to(self.comm)), got
 
     def import_nodes(self, buf, k):
+        if buf.device.type != "cuda":
+            buf = buf.to(self.device)
         self.state.import_(buf.data_ptr(), k)
