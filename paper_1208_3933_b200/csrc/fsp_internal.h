@@ -9,12 +9,12 @@
 #include "fsp.h"
 
 // Per-(couple, position) record of the pair walk, staged in shared memory.
-//   c1   = p_{j,k} + lag_j(k,l)  = sum_{k<=i<l} p_{j,i}        (int32; s16 walk:
+//   c1   = y = lag_j(k,l) + p_{j,l} = sum_{k<i<=l} p_{j,i}     (int32; s16 walk:
 //          low half, job id j in the high half)
-//   meta = (c2 << 16) | addr_j   (int32 walk)  or  (addr_j << 16) | (c2 & 0xffff) (s16 walk)
-//   c2 = p_{j,k} - p_{j,l} (int16); addr_j = shared-window address of U[j][warp 0]
+//   meta = (x << 16) | addr_j   (int32 walk)  or  (addr_j << 16) | (x & 0xffff) (s16 walk)
+//   x = p_{j,l} - p_{j,k} (int16); addr_j = shared-window address of U[j][warp 0]
 // j is the job at this position of the couple's Johnson-with-lags order.
-// DESIGN.md §6 derives the two-constant form of Fig. 3 lines 11-15.
+// DESIGN.md §6 derives the one-update form e <- max(e + x, y) of Fig. 3 lines 11-15.
 // Padding records after the last couple of a group (walk look-ahead).
 #define FSP_REC_SLACK 8
 
@@ -25,11 +25,12 @@ struct __align__(8) fsp_rec {
 
 // Dynamic shared-memory layout of the lb kernel (byte offsets).
 struct fsp_lb_layout {
-    size_t off_u, u_bytes;     // U[(n+1)][urow_words] u32 transposed unscheduled sets:
+    size_t off_u, u_bytes;     // U[(n+1)][urow_words] u32 transposed unscheduled sets (nibble
+                               //   layout: one [(n+1)][urow_words] block per warp):
     int urow_words;            //   word warp*npl + q of job j's row = nodes q*32..q*32+31
     size_t off_ptm, ptm_bytes; // PTM int32 [n][mp4]
     size_t off_bar;            // mbarrier
-    size_t off_rt, rt_bytes;   // per warp: R[MAXM][32*npl], T[MAXM][32*npl]
+    size_t off_rt, rt_bytes;   // per warp: R, A (= R + L), Q, each [MAXM][32*npl]
     size_t off_list, list_bytes; // per warp (sparse walk): compacted records of a couple
     size_t off_tab;            // one couple group: [kl header][records]
     size_t kl_bytes, group_bytes;
@@ -50,6 +51,7 @@ struct fsp_lb_plan {
     int ctas_per_sm;
     int num_sms;
     int smem_optin;      // cudaDevAttrMaxSharedMemoryPerBlockOptin
+    int tm_cols;         // TMEM columns per CTA for the per-node R/A/Q (0: in smem)
     int grid;
     size_t smem_bytes;   // dynamic smem per CTA
 };

@@ -7,7 +7,8 @@
 //   S_j[x] = sum_{i<x} p_{j,i}
 //   a_j  = p_{j,k} + lag_j(k,l) = S_j[l]   - S_j[k]      (Johnson key, machine 1)
 //   b_j  = lag_j(k,l) + p_{j,l} = S_j[l+1] - S_j[k+1]    (Johnson key, machine 2)
-//   c1_j = a_j,   c2_j = p_{j,k} - p_{j,l}
+//   y_j  = b_j,   x_j  = p_{j,l} - p_{j,k}
+// (the walk carries e = t2 - t1: e <- max(e + x_j, y_j))
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,9 +34,12 @@ static void build_tables(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl
     }
     const size_t gbytes = pl.L.group_bytes;
     const size_t kl_bytes = pl.L.kl_bytes;
-    // shared address of U[j][warp 0]; row n is the always-empty padding row
+    // shared address of U[j][warp 0] (lane-major rows), or the offset of row j
+    // in a warp's block (nibble rows, s16 with >= 10 machines: the kernel adds
+    // the block base); row n is the always-empty padding row
+    const bool nib = pl.s16 && pl.maxm >= 10; // = ULayout::NIB in lb_kernel.cu
     auto uaddr = [&](int j) {
-        return (uint32_t)(pl.smem_base + pl.L.off_u + (size_t)j * 4 * pl.L.urow_words);
+        return (uint32_t)((nib ? 0 : pl.smem_base + pl.L.off_u) + (size_t)j * 4 * pl.L.urow_words);
     };
     blob.assign(gbytes * pl.groups, 0);
     for (int g = 0; g < pl.groups; ++g) { // every record slot starts as padding
@@ -70,12 +74,12 @@ static void build_tables(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl
             fsp_rec *rec = reinterpret_cast<fsp_rec *>(gb + kl_bytes) + (size_t)pl_idx * pl.nrec;
             for (int i = 0; i < n; ++i) {
                 const int j = order[i];
-                const int c2 = ptm[(size_t)j * m + k] - ptm[(size_t)j * m + l];
-                // s16 walk: c1 < 2^15 in the low half, the job id in the high
+                const int x = ptm[(size_t)j * m + l] - ptm[(size_t)j * m + k];
+                // s16 walk: y < 2^15 in the low half, the job id in the high
                 // half (read by the sparse walk's compaction only)
-                rec[i].c1 = pl.s16 ? (int32_t)(((uint32_t)j << 16) | (uint32_t)A[j]) : A[j];
-                rec[i].meta = pl.s16 ? (int32_t)((uaddr(j) << 16) | ((uint32_t)c2 & 0xffffu))
-                                     : (int32_t)(((uint32_t)c2 << 16) | uaddr(j));
+                rec[i].c1 = pl.s16 ? (int32_t)(((uint32_t)j << 16) | (uint32_t)B[j]) : B[j];
+                rec[i].meta = pl.s16 ? (int32_t)((uaddr(j) << 16) | ((uint32_t)x & 0xffffu))
+                                     : (int32_t)(((uint32_t)x << 16) | uaddr(j));
             }
         }
     }

@@ -13,9 +13,11 @@
 //     U[job][warp] = {bits of nodes 0-31, bits of nodes 32-63}, built from
 //     coalesced reads of the prefix records; each record carries the absolute
 //     shared address of U[job][0], so one LOP3 (| 8*warp) addresses it;
-//   * the walk of Fig. 3 lines 08-17 is carried in the (u, w) form
-//         u <- max(u, w + c1_j);  w <- w + c2_j      (if j unscheduled)
-//     two predicated integer ops per update (VIADDMNMX + LEA.HI), exact int32.
+//   * the walk of Fig. 3 lines 08-17 is carried in the difference form
+//     e = timeOnM2 - timeOnM1:
+//         e <- max(e + x_j, y_j)      (if j unscheduled)
+//     x_j = p_jl - p_jk, y_j = lag_j + p_jl: one predicated VIADDMNMX per
+//     update, exact integer arithmetic.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -86,6 +88,64 @@ __device__ __forceinline__ void bulk_copy(void *dst, const void *src, uint32_t b
     }
 }
 
+// ---- tensor memory (TMEM) as per-thread scratch: the per-node R/A/Q values
+// of the walk live there instead of in shared memory ----
+__device__ __forceinline__ void tm_alloc(uint32_t *dst, uint32_t cols)
+{
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+                 "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tm_dealloc(uint32_t taddr, uint32_t cols)
+{
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tm_st1(uint32_t taddr, uint32_t v)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void tm_wait_st()
+{
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// N consecutive columns of this warp's lane quarter; the wait takes the
+// registers as operands so no use is scheduled before the data has arrived
+template <int N>
+__device__ __forceinline__ void tm_ld(uint32_t taddr, uint32_t (&v)[N])
+{
+    if constexpr (N == 2) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                     : "=r"(v[0]), "=r"(v[1])
+                     : "r"(taddr));
+    } else {
+        static_assert(N == 4, "2 or 4 columns");
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                     : "r"(taddr));
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void tm_wait_ld(uint32_t (&a)[N], uint32_t (&b)[N])
+{
+    if constexpr (N == 2) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;"
+                     : "+r"(a[0]), "+r"(a[1]), "+r"(b[0]), "+r"(b[1])::"memory");
+    } else {
+        asm volatile("tcgen05.wait::ld.sync.aligned;"
+                     : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(b[0]), "+r"(b[1]),
+                       "+r"(b[2]), "+r"(b[3])::"memory");
+    }
+}
+
+__device__ __forceinline__ int tm_half(uint32_t w, int hi) { return (int)((w >> (hi ? 16 : 0)) & 0xffffu); }
+
 struct LbArgs {
     const uint8_t *tables; // groups x group_bytes
     const int32_t *ptm;    // [n][mp4] int32, ptm_bytes
@@ -104,6 +164,7 @@ struct LbArgs {
     const int32_t *cin;    // optional prefix completion times [pool][cin_stride]
     int cin_stride;
     int vec_rows;          // vectorised scheduled-set build (long prefixes)
+    uint32_t tm_cols;      // TMEM columns allocated per CTA (TM variants)
 };
 
 // Shared address of U[job][warp] from a record's meta word (wst = 4*NPL*warp).
@@ -125,14 +186,16 @@ __device__ __forceinline__ uint32_t mask_addr(uint32_t meta, uint32_t wst, uint3
 // U row layouts (one row per job, one segment per warp):
 //  * lane-major (int32 walk): NPL words, bit L of word q = node q*32+L;
 //  * nibble (s16 walk): lane L owns NPL+1 consecutive bits of word L/LPW at
-//    shift (L % LPW)*(NPL+1); bit 1+q = node q*32+L (bit 0 stays clear).  A
-//    lane loads one word, shifts once, and R2P turns its NPL bits into the
-//    predicates P1..P4 of the updates (instead of one LOP3 per node: the ALU
-//    pipe is the walk's bottleneck).
+//    shift 1 + (L % LPW)*(NPL+1); bit 1+q of the field = node q*32+L (bit 0 of
+//    the field and bit 0 of the word stay clear, so every lane's shift is >= 1
+//    and can be a multiply-high).  A lane loads one word, shifts once, and R2P
+//    turns its NPL bits into the predicates P1..P4 of the updates (instead of
+//    one LOP3 per node: the ALU pipe is the walk's bottleneck).
 template <int NPL>
 struct Nib {
-    static constexpr int LPW = 32 / (NPL + 1);         // lanes per word
-    static constexpr int WPR = (32 + LPW - 1) / LPW;   // words per warp segment
+    static constexpr int FO = 2;                              // first node bit of lane 0
+    static constexpr int LPW = (32 - FO + 1) / (NPL + 1);     // lanes per word
+    static constexpr int WPR = (32 + LPW - 1) / LPW;          // words per warp segment
 };
 
 template <bool S16, int NPL, int MAXM>
@@ -142,7 +205,7 @@ struct ULayout {
     static constexpr bool NIB = S16 && MAXM >= 10;
     static constexpr int WPR = NIB ? Nib<NPL>::WPR : NPL;
     __device__ static int word(int L, int q) { return NIB ? L / Nib<NPL>::LPW : q; }
-    __device__ static int bit(int L, int q) { return NIB ? (L % Nib<NPL>::LPW) * (NPL + 1) + 1 + q : L; }
+    __device__ static int bit(int L, int q) { return NIB ? (L % Nib<NPL>::LPW) * (NPL + 1) + Nib<NPL>::FO + q : L; }
 };
 
 // The NPL unscheduled-bit words of one job for this warp's NPL*32 nodes.
@@ -168,25 +231,22 @@ __device__ __forceinline__ Mask<NPL> lds_mask(uint32_t addr)
     return v;
 }
 
-// One update of Fig. 3 lines 10-15 in the (u, w) form for one node; line 10
+// One update of Fig. 3 lines 10-15 for one node in the difference form
+// e = t2 - t1:  t1 += p_jk;  t2 = max(t2, t1 + lag_j) + p_jl
+// is  e = max(e + x_j, y_j)  with x_j = p_jl - p_jk, y_j = lag_j + p_jl.  Line 10
 // ("job not yet scheduled") is the predicate (a short branch ptxas predicates).
-//   int32: u = max(u, w + c1);  w += c2 (top half of meta, LEA.HI.SX32)
-//   s16:   the low halfwords carry u and w (all values fit int16, host-checked);
-//          u = max.s16(u, w + c1) (VIADDMNMX.S16x2), w += meta (low half += c2,
-//          the high halves only collect garbage that never reaches the low ones)
+//   int32: e = max(e + x, y)  (x = top half of meta, extracted once per position)
+//   s16:   the low halfword carries e (0 <= e <= t2 fits int16, host-checked):
+//          e = max.s16(e + meta, c1) (VIADDMNMX.S16x2; the low halves are x and
+//          y, the high halves only collect garbage that never reaches the low one)
 template <bool S16>
-__device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1, uint32_t meta,
-                                    int &u, int &w)
+__device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1, uint32_t x,
+                                    int &e)
 {
     if (bits & lanebit) {
-        asm volatile(""); // keep the branch so ptxas predicates the two ops
-        if constexpr (S16) {
-            u = (int)__viaddmax_s16x2((unsigned)w, c1, (unsigned)u);
-            w += (int)meta;
-        } else {
-            u = max(u, w + (int)c1);
-            w += ((int)meta >> 16);
-        }
+        asm volatile(""); // keep the branch so ptxas predicates the op
+        if constexpr (S16) e = (int)__viaddmax_s16x2((unsigned)e, x, c1);
+        else e = __viaddmax_s32(e, (int)x, (int)c1);
     }
 }
 
@@ -194,13 +254,14 @@ __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1
 #define FSP_MASK(META) lds_mask<MW>(mask_addr<S16>((META), wst, hi_mul, wst64))
 #define FSP_UPD(MASK, C1, META)                                                 \
     {                                                                           \
+        const uint32_t x_ = S16 ? (META) : (uint32_t)((int)(META) >> 16);       \
         if constexpr (UL::NIB) {                                                \
-            const uint32_t nb_ = (MASK).b[0] >> lsh;                            \
+            const uint32_t nb_ = __umulhi((MASK).b[0], shmul);                  \
             _Pragma("unroll") for (int q_ = 0; q_ < NPL; ++q_)                  \
-                upd<S16>(nb_, 2u << q_, (C1), (META), uu[q_], ww[q_]);          \
+                upd<S16>(nb_, 2u << q_, (C1), x_, ee[q_]);                      \
         } else {                                                                \
             _Pragma("unroll") for (int q_ = 0; q_ < NPL; ++q_)                  \
-                upd<S16>((MASK).b[q_], lanebit, (C1), (META), uu[q_], ww[q_]);  \
+                upd<S16>((MASK).b[q_], lanebit, (C1), x_, ee[q_]);              \
         }                                                                       \
     }
 
@@ -213,14 +274,20 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int W = blockDim.x >> 5;
     constexpr int TN = 32 * NPL;                                         // nodes per warp
-    uint32_t *Uw = reinterpret_cast<uint32_t *>(smem + a.L.off_u);      // [(n+1)][W][NPL]
+    // U: lane-major rows [(n+1)][W][NPL] (records hold absolute addresses), or,
+    // nibble layout, one block per warp [W][(n+1)][urow] (records hold the row
+    // offset, the warp's block base is added per visit: no 64 KB limit on W)
+    uint32_t *Uw = reinterpret_cast<uint32_t *>(smem + a.L.off_u) +
+                   (ULayout<S16, NPL, MAXM>::NIB ? (size_t)warp * (n + 1) * a.L.urow_words : 0);
     const int32_t *s_ptm = reinterpret_cast<const int32_t *>(smem + a.L.off_ptm);
     uint64_t *s_bar = reinterpret_cast<uint64_t *>(smem + a.L.off_bar);
-    // per-warp heads R[MAXM][TN] and tail+load T[MAXM][TN]; int16 in the s16
-    // walk (all values fit, host-checked), int32 otherwise
+    // per-warp heads R[MAXM][TN], A = R + L [MAXM][TN] (L_k = sum of p_jk over
+    // the unscheduled jobs) and tails Q[MAXM][TN]; int16 in the s16 walk (all
+    // values fit, host-checked), int32 otherwise
     using rt_t = typename std::conditional<S16, int16_t, int32_t>::type;
     rt_t *Rs = reinterpret_cast<rt_t *>(smem + a.L.off_rt + (size_t)warp * a.L.rt_bytes);
-    rt_t *Ts = Rs + MAXM * TN;
+    rt_t *As = Rs + MAXM * TN;
+    rt_t *Qs = As + MAXM * TN;
     uint8_t *s_tab = smem + a.L.off_tab;
     // SPARSE: per-warp list of the couple's records whose job is unscheduled in
     // at least one of the warp's nodes (the walk over the others is a no-op)
@@ -229,6 +296,17 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     if (smem_u32(smem) != a.smem_base) { // records carry absolute shared addresses
         if (threadIdx.x == 0) atomicOr(a.err, 2);
         return;
+    }
+    // TM: the per-node R, A, Q of phase A go to tensor memory, two machines per
+    // 32-bit column (16-bit values): column (arr*HM + k/2)*NPL + q of this
+    // warp's block in its lane quarter (warp % 4), blocks of TCOLS columns
+    constexpr bool TM = ULayout<S16, NPL, MAXM>::NIB;
+    constexpr int NPLP = NPL; // TMEM columns per (array, machine pair)
+    constexpr int HM = (MAXM + 1) / 2, TCOLS = 3 * HM * NPLP;
+    uint32_t *s_tm = reinterpret_cast<uint32_t *>(s_bar + 1);
+    if constexpr (TM) {
+        if (warp == 0) tm_alloc(s_tm, a.tm_cols);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     }
 
     auto group_size = [&](int g) {
@@ -250,6 +328,11 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
         bulk_copy(smem + a.L.off_ptm, a.ptm, (uint32_t)a.L.ptm_bytes, s_bar);
     }
     __syncthreads();
+    uint32_t tbase = 0;
+    if constexpr (TM) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tbase = *s_tm + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * TCOLS);
+    }
     uint32_t phase = 0;
     mbar_wait(s_bar, phase);
     phase ^= 1;
@@ -264,11 +347,15 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     constexpr int MW = UL::NIB ? 1 : NPL;        // mask words a lane loads
     const int lw = UL::word(lane, 0);            // nibble layout: this lane's word
     const int lsh = UL::NIB ? UL::bit(lane, 0) - 1 : 0; // ... and bit offset
-    const uint32_t wst = 4u * (WPR * warp + (UL::NIB ? lw : 0));
+    // nibble layout: the shift (lsh >= 1) that brings this lane's NPL bits to
+    // bits 1..NPL (R2P -> P1..P4), done as a multiply-high by 2^(32 - lsh) on the
+    // FMA pipe (the ALU pipe, which runs the updates, is the walk's bottleneck)
+    const uint32_t shmul = 1u << (32 - lsh);
+    const uint32_t wst = UL::NIB ? smem_u32(Uw) + 4u * lw : 4u * (WPR * warp);
     const int urow = a.L.urow_words; // words per job row of U (padded against bank conflicts)
     const uint32_t hi_mul = a.hi_mul;
     const uint64_t wst64 = (uint64_t)wst << 32;
-    const int useg = WPR * warp; // this warp's segment of a U row
+    const int useg = UL::NIB ? 0 : WPR * warp; // this warp's segment of a U row
 
     for (long long chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
         const long long tile = chunk * W + warp;
@@ -447,7 +534,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
             for (; i < dd; ++i) step(row[i]);
             // a2/a3: r_j0 = C_0, r_jk = max(C_k, r_j,k-1 + p_j,k-1) (R3); R_k =
             // min over unscheduled j (R5); Q_l = min_j q_jl, q_jl = sum_{i>l}
-            // p_ji (R4); L_l = sum_j p_jl closes the (u, w) walk.
+            // p_ji (R4); L_k = sum_j p_jk closes the difference walk.
             int R[MAXM], Q[MAXM], Ld[MAXM];
 #pragma unroll
             for (int k = 0; k < MAXM; ++k) {
@@ -505,15 +592,28 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                     Ld[k] = 0;
                 }
             }
+            if constexpr (TM) {
 #pragma unroll
-            for (int k = 0; k < MAXM; ++k) {
-                if (k < m) {
-                    Rs[k * TN + q * 32 + lane] = (rt_t)R[k];
-                    Ts[k * TN + q * 32 + lane] = (rt_t)(Q[k] + Ld[k]);
+                for (int kp = 0; kp < HM; ++kp) {
+                    const int k0 = 2 * kp, k1 = 2 * kp + 1 < MAXM ? 2 * kp + 1 : 2 * kp;
+                    auto pk = [](int lo, int hi) { return ((uint32_t)lo & 0xffffu) | ((uint32_t)hi << 16); };
+                    tm_st1(tbase + (0 * HM + kp) * NPLP + q, pk(R[k0], R[k1]));
+                    tm_st1(tbase + (1 * HM + kp) * NPLP + q, pk(R[k0] + Ld[k0], R[k1] + Ld[k1]));
+                    tm_st1(tbase + (2 * HM + kp) * NPLP + q, pk(Q[k0], Q[k1]));
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < MAXM; ++k) {
+                    if (k < m) {
+                        Rs[k * TN + q * 32 + lane] = (rt_t)R[k];
+                        As[k * TN + q * 32 + lane] = (rt_t)(R[k] + Ld[k]);
+                        Qs[k * TN + q * 32 + lane] = (rt_t)Q[k];
+                    }
                 }
             }
         }
         if (bad) atomicOr(a.err, 1);
+        if constexpr (TM) tm_wait_st();
         __syncwarp();
 
         // ---------------- a4/a5: couple walks (Fig. 3 lines 03-19) ----------------
@@ -543,12 +643,20 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
             for (int pl = 0; pl < np; ++pl) {
                 const uint32_t kv = kl[pl];
                 const int k = kv & 0xffff, l = kv >> 16;
-                // lines 06-07: timeOnM1 / timeOnM2 start at the RM minima
-                int uu[NPL], ww[NPL];
+                // lines 06-07: timeOnM1 / timeOnM2 start at the RM minima, so
+                // e = t2 - t1 starts at R_l - R_k (>= 0)
+                int ee[NPL];
+                if constexpr (TM) {
+                    uint32_t rl[NPLP], rk[NPLP];
+                    tm_ld<NPLP>(tbase + (0 * HM + (l >> 1)) * NPLP, rl);
+                    tm_ld<NPLP>(tbase + (0 * HM + (k >> 1)) * NPLP, rk);
+                    tm_wait_ld<NPLP>(rl, rk);
 #pragma unroll
-                for (int q = 0; q < NPL; ++q) {
-                    uu[q] = Rs[l * TN + q * 32 + lane];
-                    ww[q] = Rs[k * TN + q * 32 + lane];
+                    for (int q = 0; q < NPL; ++q) ee[q] = tm_half(rl[q], l & 1) - tm_half(rk[q], k & 1);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NPL; ++q)
+                        ee[q] = (int)Rs[l * TN + q * 32 + lane] - (int)Rs[k * TN + q * 32 + lane];
                 }
                 const uint4 *rp = recs + (size_t)pl * n2;
                 int n4c = n4;
@@ -631,11 +739,22 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                 }
                 if constexpr (S16) {
 #pragma unroll
-                    for (int q = 0; q < NPL; ++q) uu[q] = (int)(int16_t)(uu[q] & 0xffff);
+                    for (int q = 0; q < NPL; ++q) ee[q] = (int)(int16_t)(ee[q] & 0xffff);
                 }
+                // lines 18-19: timeOnM2 = t1 + e with t1 = R_k + L_k at the end
+                if constexpr (TM) {
+                    uint32_t ak[NPLP], ql[NPLP];
+                    tm_ld<NPLP>(tbase + (1 * HM + (k >> 1)) * NPLP, ak);
+                    tm_ld<NPLP>(tbase + (2 * HM + (l >> 1)) * NPLP, ql);
+                    tm_wait_ld<NPLP>(ak, ql);
 #pragma unroll
-                for (int q = 0; q < NPL; ++q) // lines 18-19
-                    lb[q] = max(lb[q], uu[q] + Ts[l * TN + q * 32 + lane]);
+                    for (int q = 0; q < NPL; ++q)
+                        lb[q] = max(lb[q], ee[q] + tm_half(ak[q], k & 1) + tm_half(ql[q], l & 1));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NPL; ++q)
+                        lb[q] = max(lb[q], ee[q] + As[k * TN + q * 32 + lane] + Qs[l * TN + q * 32 + lane]);
+                }
                 if constexpr (SPARSE)
                     if (compact) __syncwarp(); // the next couple rewrites s_list
             }
@@ -646,6 +765,12 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
             if (node < pool) a.lb_out[node] = lb[q];
         }
         __syncwarp();
+    }
+    if constexpr (TM) { // every warp is done with its columns
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (warp == 0) tm_dealloc(*s_tm, a.tm_cols);
     }
 }
 
@@ -743,9 +868,9 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     fsp_lb_plan &pl = sparse ? inst->plan_bb : inst->plan;
     const int n = inst->n, m = inst->m, P = inst->P;
     pl.exact = (m == 5 || m == 10 || m == 20);
-    // 16-bit walk when every walk value fits int16: t2 <= (n+m-1)*max p and
-    // w >= -n*max p
-    pl.s16 = (int64_t)(n + m - 1) * inst->max_p <= 32767 && (int64_t)n * inst->max_p <= 32767;
+    // 16-bit walk when every walk value fits int16: 0 <= e <= t2 <= (n+m-1)*max p,
+    // e + x >= -max p, and R, A, Q are bounded by t2
+    pl.s16 = (int64_t)(n + m - 1) * inst->max_p <= 32767;
     if (const char *s = getenv("FSP_LB_S16")) pl.s16 = pl.s16 && atoi(s) != 0;
     // sparse walk: exact-m s16 specialisations (records carry the job id),
     // 64 <= n <= 1024 (below 64 jobs the compaction does not pay: measured)
@@ -796,17 +921,29 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
             // s16: nibble rows (one word per lane, ceil(32/LPW) words per warp);
             // made odd so the 32 jobs a warp clears at once hit 32 banks
             const bool nib = pl.s16 && pl.maxm >= 10; // = ULayout::NIB
-            const int lpw = 32 / (npl + 1), wpr = nib ? (32 + lpw - 1) / lpw : npl;
-            const int urow = nib ? (wpr * W) | 1 : npl * W;
-            if (pl.smem_base + (size_t)(n + 1) * 4 * urow > 65536) continue; // 16-bit U addresses
+            const int lpw = 31 / (npl + 1), wpr = nib ? (32 + lpw - 1) / lpw : npl; // = Nib<npl>
+            // nibble: per-warp blocks of (n+1) rows of wpr|1 words (odd: the 32 jobs a
+            // warp clears at once hit 32 banks); record offsets j*4*urow < 64 KB
+            const int urow = nib ? wpr | 1 : npl * W;
+            if (!nib && pl.smem_base + (size_t)(n + 1) * 4 * urow > 65536) continue; // 16-bit U addresses
+            if (nib && (size_t)(n + 1) * 4 * urow > 65535) continue;
             fsp_lb_layout L{};
             L.urow_words = urow;
-            L.u_bytes = align16((size_t)(n + 1) * 4 * urow);
+            L.u_bytes = align16((size_t)(nib ? W : 1) * (n + 1) * 4 * urow);
             L.off_u = 0;
             L.ptm_bytes = align16((size_t)n * mp4 * 4);
             L.off_ptm = L.u_bytes;
             L.off_bar = L.off_ptm + L.ptm_bytes;
-            L.rt_bytes = 2 * (size_t)pl.maxm * 32 * npl * (pl.s16 ? 2 : 4);
+            // nibble variants keep R/A/Q in TMEM: ceil(W/4) blocks of 3*ceil(maxm/2)*npl
+            // columns per lane quarter, allocated as a power of two >= 32 per CTA
+            int tm_cols = 0;
+            if (nib) {
+                const int need = (W + 3) / 4 * 3 * ((pl.maxm + 1) / 2) * npl;
+                tm_cols = 32;
+                while (tm_cols < need) tm_cols *= 2;
+                if (tm_cols > 512) continue;
+            }
+            L.rt_bytes = nib ? 0 : 3 * (size_t)pl.maxm * 32 * npl * (pl.s16 ? 2 : 4);
             L.off_rt = L.off_bar + 16;
             L.list_bytes = pl.sparse ? align16(((size_t)pl.nrec + FSP_REC_SLACK + 4) * 8) : 0;
             L.off_list = align16(L.off_rt + (size_t)W * L.rt_bytes);
@@ -827,7 +964,11 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                     c.pairs_per_group = ppg;
                     c.warps = W;
                     c.smem_bytes = L.off_tab + gb;
-                    if (occupancy_of(c) == FSP_OK && c.ctas_per_sm > 0) {
+                    c.tm_cols = tm_cols;
+                    // co-resident CTAs must fit the SM's 512 TMEM columns (an
+                    // allocation beyond them would wait for another CTA to exit)
+                    if (occupancy_of(c) == FSP_OK && c.ctas_per_sm > 0 &&
+                        c.ctas_per_sm * tm_cols <= 512) {
                         const double score = (double)W * c.ctas_per_sm * (npl == 4 ? 1.5 : 1.0) /
                                              (1.0 + 0.015 * (Greal - 1));
                         if (score > best) {
@@ -886,5 +1027,6 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.nrec = pl.nrec;
     a.stride = stride;
     a.hi_mul = 0x10000u;
+    a.tm_cols = (uint32_t)pl.tm_cols;
     FSP_DISPATCH(launch, pl, a, s);
 }
