@@ -23,6 +23,12 @@ struct __align__(8) fsp_rec {
     int32_t meta;
 };
 
+// u32 words per job of the packed machine-pair rows [p pairs][q pairs] that the
+// nibble (TMEM) variants of the lb kernel stage after PTM: p pair = p_{j,2i} |
+// p_{j,2i+1} << 16, q pair the same for the tails q_jl = sum_{i>l} p_ji; each
+// half padded from ceil(maxm/2) to a multiple of 4 words.
+static inline int fsp_pq_words(int maxm) { return 2 * ((((maxm + 1) / 2) + 3) & ~3); }
+
 // Dynamic shared-memory layout of the lb kernel (byte offsets).
 struct fsp_lb_layout {
     size_t off_u, u_bytes;     // U[(n+1)][urow_words] u32 transposed unscheduled sets (nibble

@@ -135,6 +135,19 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
     std::vector<int32_t> p32(pl.L.ptm_bytes / 4, 0);
     for (int j = 0; j < n; ++j)
         for (int k = 0; k < m; ++k) p32[(size_t)j * mp4 + k] = ptm[(size_t)j * m + k];
+    if (pl.s16 && pl.maxm >= 10) { // nibble/TMEM variants: packed (p, q) machine pairs
+        const int W = fsp_pq_words(pl.maxm), H = W / 2;
+        uint32_t *pq = reinterpret_cast<uint32_t *>(p32.data() + (size_t)n * mp4);
+        for (int j = 0; j < n; ++j) {
+            std::vector<int32_t> pj(pl.maxm + 1, 0), qj(pl.maxm + 1, 0);
+            for (int k = 0; k < m; ++k) pj[k] = ptm[(size_t)j * m + k];
+            for (int l = m - 2; l >= 0; --l) qj[l] = qj[l + 1] + pj[l + 1]; // q_jl = sum_{i>l} p_ji
+            for (int kp = 0; 2 * kp < m; ++kp) {
+                pq[(size_t)j * W + kp] = (uint32_t)pj[2 * kp] | ((uint32_t)pj[2 * kp + 1] << 16);
+                pq[(size_t)j * W + H + kp] = (uint32_t)qj[2 * kp] | ((uint32_t)qj[2 * kp + 1] << 16);
+            }
+        }
+    }
 
     inst->table_bytes = (int64_t)blob.size();
     e = cudaMalloc(&inst->d_tables, blob.size());

@@ -280,6 +280,8 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     uint32_t *Uw = reinterpret_cast<uint32_t *>(smem + a.L.off_u) +
                    (ULayout<S16, NPL, MAXM>::NIB ? (size_t)warp * (n + 1) * a.L.urow_words : 0);
     const int32_t *s_ptm = reinterpret_cast<const int32_t *>(smem + a.L.off_ptm);
+    // TM variants: per job [p pairs x HMP][q pairs x HMP] u32 after PTM (see fsp_plan_lb)
+    const uint32_t *s_pq = reinterpret_cast<const uint32_t *>(s_ptm + (size_t)a.n * a.mp4);
     uint64_t *s_bar = reinterpret_cast<uint64_t *>(smem + a.L.off_bar);
     // per-warp heads R[MAXM][TN], A = R + L [MAXM][TN] (L_k = sum of p_jk over
     // the unscheduled jobs) and tails Q[MAXM][TN]; int16 in the s16 walk (all
@@ -303,6 +305,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     constexpr bool TM = ULayout<S16, NPL, MAXM>::NIB;
     constexpr int NPLP = NPL; // TMEM columns per (array, machine pair)
     constexpr int HM = (MAXM + 1) / 2, TCOLS = 3 * HM * NPLP;
+    constexpr int HMP = (HM + 3) & ~3; // machine pairs per packed row, padded to 16 bytes
     uint32_t *s_tm = reinterpret_cast<uint32_t *>(s_bar + 1);
     if constexpr (TM) {
         if (warp == 0) tm_alloc(s_tm, a.tm_cols);
@@ -535,12 +538,22 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
             // a2/a3: r_j0 = C_0, r_jk = max(C_k, r_j,k-1 + p_j,k-1) (R3); R_k =
             // min over unscheduled j (R5); Q_l = min_j q_jl, q_jl = sum_{i>l}
             // p_ji (R4); L_k = sum_j p_jk closes the difference walk.
+            // TM variants keep Q and L as packed 16-bit machine pairs (all values
+            // are < 2^15, host-checked): tails q_jl come from a per-job table of
+            // machine pairs (one VIMNMX.U16x2 per pair) and p_jl from another
+            // (one add per pair), next to PTM in shared memory
             int R[MAXM], Q[MAXM], Ld[MAXM];
+            uint32_t Q2[HM], L2[HM];
 #pragma unroll
             for (int k = 0; k < MAXM; ++k) {
                 R[k] = INT_MAX;
                 Q[k] = INT_MAX;
                 Ld[k] = 0;
+            }
+#pragma unroll
+            for (int kp = 0; kp < HM; ++kp) {
+                Q2[kp] = 0xffffffffu;
+                L2[kp] = 0;
             }
             int cnt = 0;
             for (int j = 0; j < n; ++j) {
@@ -572,13 +585,29 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                             R[k] = min(R[k], r);
                         }
                     }
-                    int qq = 0;
+                    if constexpr (TM) {
+                        const uint4 *pq = reinterpret_cast<const uint4 *>(s_pq + j * 2 * HMP);
 #pragma unroll
-                    for (int l = MAXM - 1; l >= 0; --l) {
-                        if (l < m) {
-                            Q[l] = min(Q[l], qq);
-                            qq += p[l];
-                            Ld[l] += p[l];
+                        for (int c4 = 0; c4 < HMP / 4; ++c4) {
+                            const uint4 pv = pq[c4], qv = pq[HMP / 4 + c4];
+                            const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                if (4 * c4 + t < HM) {
+                                    Q2[4 * c4 + t] = __vminu2(Q2[4 * c4 + t], qw[t]);
+                                    L2[4 * c4 + t] += pw[t];
+                                }
+                            }
+                        }
+                    } else {
+                        int qq = 0;
+#pragma unroll
+                        for (int l = MAXM - 1; l >= 0; --l) {
+                            if (l < m) {
+                                Q[l] = min(Q[l], qq);
+                                qq += p[l];
+                                Ld[l] += p[l];
+                            }
                         }
                     }
                 }
@@ -591,6 +620,11 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                     Q[k] = 0;
                     Ld[k] = 0;
                 }
+#pragma unroll
+                for (int kp = 0; kp < HM; ++kp) {
+                    Q2[kp] = 0;
+                    L2[kp] = 0;
+                }
             }
             if constexpr (TM) {
 #pragma unroll
@@ -598,8 +632,8 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                     const int k0 = 2 * kp, k1 = 2 * kp + 1 < MAXM ? 2 * kp + 1 : 2 * kp;
                     auto pk = [](int lo, int hi) { return ((uint32_t)lo & 0xffffu) | ((uint32_t)hi << 16); };
                     tm_st1(tbase + (0 * HM + kp) * NPLP + q, pk(R[k0], R[k1]));
-                    tm_st1(tbase + (1 * HM + kp) * NPLP + q, pk(R[k0] + Ld[k0], R[k1] + Ld[k1]));
-                    tm_st1(tbase + (2 * HM + kp) * NPLP + q, pk(Q[k0], Q[k1]));
+                    tm_st1(tbase + (1 * HM + kp) * NPLP + q, pk(R[k0], R[k1]) + L2[kp]); // A = R + L
+                    tm_st1(tbase + (2 * HM + kp) * NPLP + q, Q2[kp]);
                 }
             } else {
 #pragma unroll
@@ -931,7 +965,8 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
             L.urow_words = urow;
             L.u_bytes = align16((size_t)(nib ? W : 1) * (n + 1) * 4 * urow);
             L.off_u = 0;
-            L.ptm_bytes = align16((size_t)n * mp4 * 4);
+            // + the packed (p, q) machine-pair rows of the TM (nibble) variants
+            L.ptm_bytes = align16((size_t)n * mp4 * 4) + (nib ? (size_t)n * fsp_pq_words(pl.maxm) * 4 : 0);
             L.off_ptm = L.u_bytes;
             L.off_bar = L.off_ptm + L.ptm_bytes;
             // nibble variants keep R/A/Q in TMEM: ceil(W/4) blocks of 3*ceil(maxm/2)*npl
