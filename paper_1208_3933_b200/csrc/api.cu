@@ -131,12 +131,14 @@ extern "C" int fsp_lb_eval_host(const fsp_instance *inst, const uint16_t *prefix
     HostCtx *c = static_cast<HostCtx *>(mi->host_ctx);
     std::lock_guard<std::mutex> g(c->mu);
 
-    // chunk: whole waves of the persistent kernel (grid x warps x 32 x nodes
-    // per lane nodes) closest to 2^18, so every chunk keeps every SM busy and
-    // the copies of chunk i+1 overlap the kernel of chunk i
+    // chunk: about an eighth of the pool (2^16 .. 2^20 nodes, whole warp tiles),
+    // so the copies of chunk i+1 overlap the kernel of chunk i and the first
+    // copy, which nothing overlaps, stays short; the kernel spreads the tiles of
+    // a chunk over every SM (a partial wave leaves warps idle, not SMs)
     const fsp_lb_plan &pl = inst->plan;
-    const int64_t wave = (int64_t)pl.grid * pl.warps * 32 * pl.npl;
-    int64_t chunk = wave * std::max<int64_t>(1, ((1 << 18) + wave / 2) / wave);
+    const int64_t tile = 32 * pl.npl;
+    int64_t chunk = std::min<int64_t>(1 << 20, std::max<int64_t>(1 << 16, (pool + 7) / 8));
+    chunk = (chunk + tile - 1) / tile * tile;
     if (chunk > pool) chunk = pool;
     if (c->cap_nodes < chunk || c->cap_stride < stride) {
         for (int s = 0; s < 2; ++s) {

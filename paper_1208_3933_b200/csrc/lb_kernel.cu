@@ -343,7 +343,10 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
 
     const long long pool = a.pool_dev ? *a.pool_dev : a.pool;
     const long long ntiles = (pool + TN - 1) / TN;
-    const long long nchunks = (ntiles + W - 1) / W;
+    // iteration `it` of CTA b takes tiles (it*W + warp)*grid + b: the tiles of a
+    // partial last iteration spread over every SM (a few idle warps per CTA)
+    // instead of leaving whole SMs idle
+    const long long niter = (ntiles + (long long)W * gridDim.x - 1) / ((long long)W * gridDim.x);
     const uint32_t lanebit = 1u << lane;
     using UL = ULayout<S16, NPL, MAXM>;
     constexpr int WPR = UL::WPR;                 // U words per warp per job row
@@ -360,8 +363,8 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     const uint64_t wst64 = (uint64_t)wst << 32;
     const int useg = UL::NIB ? 0 : WPR * warp; // this warp's segment of a U row
 
-    for (long long chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
-        const long long tile = chunk * W + warp;
+    for (long long it = 0; it < niter; ++it) {
+        const long long tile = (it * W + warp) * gridDim.x + blockIdx.x;
         bool bad = false;
 
         // ---------------- a1: node ingest (depth, scheduled set) ----------------
