@@ -374,13 +374,15 @@ __global__ void __launch_bounds__(kPruneThreads)
         st.lb[dst] = ch.lb[i];
     }
     __syncthreads();
-    // warp-cooperative, coalesced row copies
+    // warp-cooperative, coalesced row copies; rows are 16-byte aligned (stride
+    // is a multiple of 8), so prefixes move as uint4s (eight job ids each)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
     for (int k = wib; k < tot; k += nwb) {
         const int64_t src = s_src[k], dst = s_dst[k];
-        const int dd = ch.dp[src];
-        for (int q = lane; q < dd; q += 32)
-            st.pf[(size_t)dst * stride + q] = ch.pf[(size_t)src * stride + q];
+        const int d8 = (ch.dp[src] + 7) >> 3;
+        const uint4 *srow = reinterpret_cast<const uint4 *>(ch.pf + (size_t)src * stride);
+        uint4 *drow = reinterpret_cast<uint4 *>(st.pf + (size_t)dst * stride);
+        for (int q = lane; q < d8; q += 32) drow[q] = srow[q];
         for (int q = lane; q < m; q += 32) st.C[(size_t)dst * m + q] = ch.C[(size_t)src * m + q];
     }
 }
