@@ -3,6 +3,7 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config ta091] [--pool NODES_PER_GPU] [--no-e2e] [--no-bb]
+  python bench.py --table2     (the paper's Table II protocol on B&B frontier pools)
 
 One step = one fsp_lb_eval over the whole per-GPU pool (every row a1-a5 of
 SURVEY.md §8(a) runs inside the kernel), pool resident in HBM.  Under torchrun
@@ -43,6 +44,8 @@ def parse():
     ap.add_argument("--no-bb", action="store_true")
     ap.add_argument("--bb-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--table2", action="store_true",
+                    help="Table II grid: Tcpu/Tgpu per instance class and pool size")
     return ap.parse_args()
 
 
@@ -229,10 +232,113 @@ def run_reference(a):
     print(json.dumps(out), flush=True)
 
 
+TABLE2_SIZES = [4096, 8192, 16384, 32768, 65536, 131072, 262144, 1048576]
+TABLE2_CFGS = ["ta021", "ta051", "c100x20", "ta091"]
+
+
+def frontier(binding, inst, n, seconds=5.0):
+    """The paper's list L: open sub-problems of a running B&B.  The
+    device B&B runs from the root for a fixed time box (incumbent-less start,
+    deepest-first batches) and its open nodes are exported (fsp_bb_export) as
+    the list: every depth the search holds open, shallow to deep."""
+    import torch
+    bb = binding.BBState(inst)
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds and bb.pool_size() > 0:
+        bb.step(8)
+    k = bb.pool_size()
+    nb = bb.node_bytes()
+    buf = torch.empty(max(1, k) * nb, dtype=torch.uint8, device="cuda")
+    k = bb.export(k, buf.data_ptr())
+    stride = (n + 7) & ~7
+    h = buf[: k * nb].cpu().numpy()
+    pf = h[: k * stride * 2].view(np.uint16).reshape(k, stride).copy()
+    dp = h[k * stride * 2: k * stride * 2 + 4 * k].view(np.int32).copy()
+    st = bb.stats()
+    bb.close()
+    return pf, dp, st
+
+
+def run_table2(a):
+    """Table II of the paper on B200: for each instance class and pool
+    size, Tcpu/Tgpu of bounding a pool of sub-problems drawn from a B&B frontier.
+    Tcpu: the oracle on ONE host core (the paper's serial B&B core), timed on a
+    bounded sample and scaled per node; Tgpu: fsp_lb_eval_host (the paper's
+    offload: host pool -> GPU -> host LBs, copies timed) and fsp_lb_eval (pool
+    resident in HBM).  The sampled LBs are checked against the oracle."""
+    import torch
+
+    import oracle
+    from paper_1208_3933_b200 import binding
+    rows = []
+    for cfg in TABLE2_CFGS:
+        n, m, seed = inputs.TAILLARD_SEEDS[cfg]
+        ptm = inputs.taillard(n, m, seed)
+        inst = binding.Instance(ptm)
+        pfL, dpL, st = frontier(binding, inst, n)
+        # a random order of the list (seeded): every pool mixes its depths
+        perm = np.random.default_rng(12083933).permutation(len(dpL))
+        pfL, dpL = pfL[perm], dpL[perm]
+        L = len(dpL)
+        T = oracle.Tables(ptm)
+        # Tcpu per node: one core, a sample of the list (same depth mix)
+        samp = np.arange(min(L, 2048))
+        t0 = time.perf_counter()
+        ref = T.lb_eval(pfL[samp], dpL[samp])
+        cpu_node = (time.perf_counter() - t0) / len(samp)
+        best = None
+        for S in TABLE2_SIZES:
+            idx = np.arange(S) % L  # the list, cycled when shorter than S
+            pf, dp = np.ascontiguousarray(pfL[idx]), np.ascontiguousarray(dpL[idx])
+            stride = pf.shape[1]
+            h_pf = torch.from_numpy(pf.view(np.int16)).pin_memory()
+            h_dp = torch.from_numpy(dp).pin_memory()
+            h_lb = torch.empty(S, dtype=torch.int32).pin_memory()
+            d_pf, d_dp = h_pf.cuda(), h_dp.cuda()
+            d_lb = torch.empty(S, dtype=torch.int32, device="cuda")
+            reps = max(3, min(200, (1 << 22) // S))
+            for _ in range(2):
+                inst.lb_eval_host_ptr(h_pf.data_ptr(), stride, h_dp.data_ptr(), S, h_lb.data_ptr())
+                inst.lb_eval(d_pf, d_dp, d_lb)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                inst.lb_eval_host_ptr(h_pf.data_ptr(), stride, h_dp.data_ptr(), S, h_lb.data_ptr())
+            t_host = (time.perf_counter() - t0) / reps
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            for _ in range(reps):
+                inst.lb_eval(d_pf, d_dp, d_lb)
+            e1.record()
+            torch.cuda.synchronize()
+            t_dev = e0.elapsed_time(e1) / reps / 1e3
+            k = min(S, len(samp))
+            if not (np.array_equal(h_lb.numpy()[:k], ref[:k]) and torch.equal(h_lb, d_lb.cpu())):
+                raise SystemExit(f"table2: GPU LBs differ from the oracle ({cfg}, pool {S})")
+            tcpu = cpu_node * S
+            row = {"instance": f"{cfg}-class {n}x{m}", "pool": S, "blocks_x_256": f"{S // 256}x256",
+                   "list_nodes": L, "mean_depth": float(dpL[idx].mean()),
+                   "tcpu_ms_1core": tcpu * 1e3, "tgpu_ms_offload": t_host * 1e3,
+                   "tgpu_ms_resident": t_dev * 1e3, "tcpu_over_tgpu_offload": tcpu / t_host,
+                   "tcpu_over_tgpu_resident": tcpu / t_dev, "bounds_per_s_offload": S / t_host,
+                   "bounds_per_s_resident": S / t_dev}
+            print(json.dumps(row), flush=True)
+            rows.append(row)
+            if best is None or row["tcpu_over_tgpu_offload"] > best[1]:
+                best = (S, row["tcpu_over_tgpu_offload"])
+        print(json.dumps({"instance": f"{cfg}-class {n}x{m}", "best_pool_offload": best[0],
+                          "best_tcpu_over_tgpu_offload": best[1], "bb_iterations_for_list":
+                          st.get("iterations")}), flush=True)
+        inst.close()
+    return rows
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         return run_reference(a)
+    if a.table2:
+        return run_table2(a)
     import torch
     import torch.distributed as dist
 

@@ -30,6 +30,7 @@ TAILLARD_SEEDS = {
     "ta005": (20, 5, 495070989),
     "ta021": (20, 20, 479340445),
     "ta051": (50, 20, 1539989115),
+    "c100x20": (100, 20, 1286373166),  # 100x20 class (seed recalled for ta081, unverified)
     "ta091": (200, 20, 2013025619),
     "ta111": (500, 20, 1368624604),
 }
