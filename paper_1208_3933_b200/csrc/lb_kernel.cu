@@ -165,6 +165,8 @@ struct LbArgs {
     int cin_stride;
     int vec_rows;          // vectorised scheduled-set build (long prefixes)
     uint32_t tm_cols;      // TMEM columns allocated per CTA (TM variants)
+    int split;             // warps per tile (power of two <= W): each walks every
+                           // split-th couple, LBs combined by atomicMax (lb_out zeroed)
 };
 
 // Shared address of U[job][warp] from a record's meta word (wst = 4*NPL*warp).
@@ -346,7 +348,12 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     // iteration `it` of CTA b takes tiles (it*W + warp)*grid + b: the tiles of a
     // partial last iteration spread over every SM (a few idle warps per CTA)
     // instead of leaving whole SMs idle
-    const long long niter = (ntiles + (long long)W * gridDim.x - 1) / ((long long)W * gridDim.x);
+    // small pools (fewer tiles than warps on the GPU): `split` warps share a
+    // tile, each walking every split-th couple of a group (phase A is repeated
+    // per warp); warps split*t .. split*t+split-1 sit on different SMSPs
+    const int split = a.split, slice = warp & (split - 1);
+    const int Wt = W / split; // tiles per CTA iteration
+    const long long niter = (ntiles + (long long)Wt * gridDim.x - 1) / ((long long)Wt * gridDim.x);
     const uint32_t lanebit = 1u << lane;
     using UL = ULayout<S16, NPL, MAXM>;
     constexpr int WPR = UL::WPR;                 // U words per warp per job row
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     const int useg = UL::NIB ? 0 : WPR * warp; // this warp's segment of a U row
 
     for (long long it = 0; it < niter; ++it) {
-        const long long tile = (it * W + warp) * gridDim.x + blockIdx.x;
+        const long long tile = (it * Wt + warp / split) * gridDim.x + blockIdx.x;
         bool bad = false;
 
         // ---------------- a1: node ingest (depth, scheduled set) ----------------
@@ -677,7 +684,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
             const uint4 *recs = reinterpret_cast<const uint4 *>(s_tab + a.L.kl_bytes);
             const int np = group_size(g);
             const int n2 = a.nrec >> 1, n4 = a.nrec >> 2;
-            for (int pl = 0; pl < np; ++pl) {
+            for (int pl = slice; pl < np; pl += split) {
                 const uint32_t kv = kl[pl];
                 const int k = kv & 0xffff, l = kv >> 16;
                 // lines 06-07: timeOnM1 / timeOnM2 start at the RM minima, so
@@ -799,7 +806,10 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
             const long long node = tile * TN + q * 32 + lane;
-            if (node < pool) a.lb_out[node] = lb[q];
+            if (node < pool) {
+                if (split == 1) a.lb_out[node] = lb[q];
+                else atomicMax(&a.lb_out[node], lb[q]);
+            }
         }
         __syncwarp();
     }
@@ -1066,5 +1076,23 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.stride = stride;
     a.hi_mul = 0x10000u;
     a.tm_cols = (uint32_t)pl.tm_cols;
+    // couple split for pools with fewer tiles than warp slots (latency-bound
+    // otherwise: a 4,096-node pool is 32 tiles on 148 x 16 warps); the pool size
+    // of a device-sized launch (B&B) is only bounded by `pool`
+    a.split = 1;
+    {
+        const int64_t tiles = (pool + 32 * pl.npl - 1) / (32 * pl.npl);
+        const int64_t slots = (int64_t)pl.grid * pl.warps;
+        while (a.split < pl.warps && tiles * a.split * 2 <= slots) a.split *= 2;
+        if (const char *e = getenv("FSP_LB_SPLIT")) { // experiments: a power of two
+            const int v = std::max(1, std::min(pl.warps, atoi(e)));
+            for (a.split = 1; a.split * 2 <= v;) a.split *= 2;
+        }
+        while (pl.warps % a.split) a.split /= 2;
+    }
+    if (a.split > 1 && pool > 0) { // R1: every LB is a max starting at 0
+        cudaError_t e = cudaMemsetAsync(lb_out, 0, sizeof(int32_t) * (size_t)pool, s);
+        if (e != cudaSuccess) return fsp_cuda_fail(e, "lb_out clear");
+    }
     FSP_DISPATCH(launch, pl, a, s);
 }
