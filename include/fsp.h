@@ -87,8 +87,11 @@ int fsp_instance_get_info(const fsp_instance *inst, fsp_instance_info *info);
  *   depth   DEVICE int32 [pool], 0 <= depth[i] <= n.  depth == n returns the
  *           makespan (R6); depth == n-1 returns the exact makespan of the
  *           forced completion.
- *   lb_out  DEVICE int32 [pool]; each element written exactly once and
- *           depending only on node i (order-preserving, pure).
+ *   lb_out  DEVICE int32 [pool]; fully overwritten, element i depending only
+ *           on node i (order-preserving, pure).  Pools with fewer warp tiles
+ *           than the GPU has warp slots are cleared first (stream-ordered
+ *           memset; R1: the LB is a max from 0) and combined by atomicMax
+ *           from several warps; lb_out must not alias prefix or depth.
  *   pool    number of nodes, >= 0 (0 is a no-op).
  * Malformed nodes (job >= n, repeated job, depth outside [0,n]) never cause
  * an out-of-bounds access: their LB is unspecified and a device flag is set,
