@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     // nibble layout: the shift (lsh >= 1) that brings this lane's NPL bits to
     // bits 1..NPL (R2P -> P1..P4), done as a multiply-high by 2^(32 - lsh) on the
     // FMA pipe (the ALU pipe, which runs the updates, is the walk's bottleneck)
-    const uint32_t shmul = 1u << (32 - lsh);
+    const uint32_t shmul = UL::NIB ? 1u << (32 - lsh) : 1u;
     const uint32_t wst = UL::NIB ? smem_u32(Uw) + 4u * lw : 4u * (WPR * warp);
     const int urow = a.L.urow_words; // words per job row of U (padded against bank conflicts)
     const uint32_t hi_mul = a.hi_mul;
