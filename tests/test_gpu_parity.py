@@ -216,3 +216,19 @@ def test_parity_sibling_api_on_random_pools(torch, fsp, orc):
         for pf, dp in (inputs.pool_d1(n, N, 9), inputs.pool_fixed_depth(n, N, n - 3, 10)):
             got = inst.lb_eval_sibling(dev(torch, pf), dev(torch, dp)).cpu().numpy()
             assert (got == T.lb_eval(pf, dp)).all()
+
+
+@pytest.mark.parametrize("split", [1, 2, 4, 8, 16])
+def test_parity_couple_split(torch, fsp, orc, monkeypatch, split):
+    """Every couple split of a tile over `split` warps (LbArgs.split, atomicMax
+    combine) gives the oracle's LBs: a 200x20 pool whose 3 couple groups are
+    shared out unevenly (64 couples per group, 190 in all) and a ragged tail."""
+    monkeypatch.setenv("FSP_LB_SPLIT", str(split))
+    n, m, seed = inputs.TAILLARD_SEEDS["ta091"]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, 1500, inputs.pool_seed("ta091") + 77)
+    compare(torch, fsp, orc, ptm, pf, dp)
+    n, m, seed = inputs.TAILLARD_SEEDS["ta021"]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, 3001, inputs.pool_seed("ta021") + 77)
+    compare(torch, fsp, orc, ptm, pf, dp)
