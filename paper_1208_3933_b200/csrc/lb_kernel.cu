@@ -947,8 +947,10 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     // reload).  Env FSP_LB_NPL / FSP_LB_WARPS pin a choice (sweeps, tests).
     int npl_lo = 2, npl_hi = pl.exact ? 4 : 2;
     if (const char *s = getenv("FSP_LB_NPL")) npl_lo = npl_hi = (atoi(s) == 4 && pl.exact) ? 4 : 2;
-    // sparse walk: 64-node warps keep the union of the block's unscheduled sets small
-    if (pl.sparse) npl_lo = npl_hi = getenv("FSP_BB_NPL") && atoi(getenv("FSP_BB_NPL")) == 4 ? 4 : 2;
+    // sparse walk: 4 nodes per lane (128-node blocks) since the difference walk and
+    // TMEM heads (ta091 B&B: 390 M nodes/s vs 314 M with 64-node blocks, whose
+    // smaller live sets no longer outweigh the per-node table and mask traffic)
+    if (pl.sparse) npl_lo = npl_hi = getenv("FSP_BB_NPL") && atoi(getenv("FSP_BB_NPL")) == 2 ? 2 : 4;
     int w_lo = 1, w_hi = pl.maxm > 20 ? 8 : 16; // launch bounds of the wide variants
     if (const char *s = getenv("FSP_LB_WARPS")) w_lo = w_hi = std::max(1, std::min(w_hi, atoi(s)));
     double best = -1.0;
