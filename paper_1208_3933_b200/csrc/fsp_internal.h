@@ -35,7 +35,7 @@ struct fsp_lb_layout {
                                //   layout: one [(n+1)][urow_words] block per warp):
     int urow_words;            //   word warp*npl + q of job j's row = nodes q*32..q*32+31
     size_t off_ptm, ptm_bytes; // PTM int32 [n][mp4]
-    size_t off_bar;            // mbarrier
+    size_t off_bar;            // mbarriers, buffer release counters, TMEM address (32 B)
     size_t off_rt, rt_bytes;   // per warp: R, A (= R + L), Q, each [MAXM][32*npl]
     size_t off_list, list_bytes; // per warp (sparse walk): compacted records of a couple
     size_t off_tab;            // one couple group: [kl header][records]
@@ -53,6 +53,7 @@ struct fsp_lb_plan {
     fsp_lb_layout L;
     int groups;          // couple groups (one resident in smem at a time)
     int pairs_per_group; // couples per group (last group may be shorter)
+    bool dbuf;           // groups >= 2 double-buffered in shared memory
     int warps;           // warps per CTA
     int ctas_per_sm;
     int num_sms;

@@ -165,6 +165,7 @@ struct LbArgs {
     int cin_stride;
     int vec_rows;          // vectorised scheduled-set build (long prefixes)
     uint32_t tm_cols;      // TMEM columns allocated per CTA (TM variants)
+    int dbuf;              // couple groups double-buffered (groups >= 2): no CTA barrier
     int split;             // warps per tile (power of two <= W): each walks every
                            // split-th couple, LBs combined by atomicMax (lb_out zeroed)
 };
@@ -308,7 +309,11 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     constexpr int NPLP = NPL; // TMEM columns per (array, machine pair)
     constexpr int HM = (MAXM + 1) / 2, TCOLS = 3 * HM * NPLP;
     constexpr int HMP = (HM + 3) & ~3; // machine pairs per packed row, padded to 16 bytes
-    uint32_t *s_tm = reinterpret_cast<uint32_t *>(s_bar + 1);
+    // barrier area (32 B): [0] mbarrier "group buffer 0 full" (with PTM), [1]
+    // "buffer 1 full", [2] release counters of the two buffers (u32 x 2), [3] TMEM
+    // base address
+    uint32_t *s_cnt = reinterpret_cast<uint32_t *>(s_bar + 2);
+    uint32_t *s_tm = reinterpret_cast<uint32_t *>(s_bar + 3);
     if constexpr (TM) {
         if (warp == 0) tm_alloc(s_tm, a.tm_cols);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -324,13 +329,34 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                           ~size_t(15));
     };
 
-    // ---- stage PTM + the first couple group (TMA bulk, one mbarrier) ----
+    const long long pool = a.pool_dev ? *a.pool_dev : a.pool;
+    const long long ntiles = (pool + TN - 1) / TN;
+    // small pools (fewer tiles than warps on the GPU): `split` warps share a
+    // tile, each walking every split-th couple of a group (phase A is repeated
+    // per warp); warps split*t .. split*t+split-1 sit on different SMSPs
+    const int split = a.split, slice = warp & (split - 1);
+    const int Wt = W / split; // tiles per CTA iteration
+    const long long niter = (ntiles + (long long)Wt * gridDim.x - 1) / ((long long)Wt * gridDim.x);
+    // double-buffered couple groups: the CTA's sequence of groups is it*G + gi;
+    // group sequence number sq lives in buffer sq & 1, whose (sq >> 1)-th fill
+    // it is; the last warp to release a buffer refills it with group sq + 2
+    const bool dbuf = a.dbuf != 0;
+    const long long nseq = niter * a.groups;
+
+    // ---- stage PTM + the first couple group(s) (TMA bulk, mbarriers) ----
     if (threadIdx.x == 0) {
         mbar_init(s_bar, 1);
+        mbar_init(s_bar + 1, 1);
+        s_cnt[0] = s_cnt[1] = 0;
         uint32_t gb = group_blob(0);
         mbar_expect_tx(s_bar, gb + (uint32_t)a.L.ptm_bytes);
         bulk_copy(s_tab, a.tables, gb, s_bar);
         bulk_copy(smem + a.L.off_ptm, a.ptm, (uint32_t)a.L.ptm_bytes, s_bar);
+        if (dbuf && nseq >= 2) {
+            gb = group_blob(1);
+            mbar_expect_tx(s_bar + 1, gb);
+            bulk_copy(s_tab + a.L.group_bytes, a.tables + a.L.group_bytes, gb, s_bar + 1);
+        }
     }
     __syncthreads();
     uint32_t tbase = 0;
@@ -343,17 +369,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     phase ^= 1;
     int resident = 0;
 
-    const long long pool = a.pool_dev ? *a.pool_dev : a.pool;
-    const long long ntiles = (pool + TN - 1) / TN;
-    // iteration `it` of CTA b takes tiles (it*W + warp)*grid + b: the tiles of a
-    // partial last iteration spread over every SM (a few idle warps per CTA)
-    // instead of leaving whole SMs idle
-    // small pools (fewer tiles than warps on the GPU): `split` warps share a
-    // tile, each walking every split-th couple of a group (phase A is repeated
-    // per warp); warps split*t .. split*t+split-1 sit on different SMSPs
-    const int split = a.split, slice = warp & (split - 1);
-    const int Wt = W / split; // tiles per CTA iteration
-    const long long niter = (ntiles + (long long)Wt * gridDim.x - 1) / ((long long)Wt * gridDim.x);
+    // iteration `it` of CTA b takes tiles (it*Wt + warp/split)*grid + b: the
+    // tiles of a partial last iteration spread over every SM (a few idle warps
+    // per CTA) instead of leaving whole SMs idle
     const uint32_t lanebit = 1u << lane;
     using UL = ULayout<S16, NPL, MAXM>;
     constexpr int WPR = UL::WPR;                 // U words per warp per job row
@@ -666,8 +684,14 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
         for (int q = 0; q < NPL; ++q) lb[q] = 0;
         const bool ascending = resident == 0;
         for (int gi = 0; gi < a.groups; ++gi) {
-            const int g = ascending ? gi : a.groups - 1 - gi;
-            if (g != resident) {
+            const int g = dbuf ? gi : ascending ? gi : a.groups - 1 - gi;
+            const long long sq = it * a.groups + gi;
+            const uint8_t *tab = s_tab;
+            if (dbuf) { // wait for this group's buffer; no CTA-wide barrier
+                const int b = (int)(sq & 1);
+                mbar_wait(s_bar + b, (uint32_t)((sq >> 1) & 1));
+                tab = s_tab + (size_t)b * a.L.group_bytes;
+            } else if (g != resident) {
                 __syncthreads(); // every warp is done with the resident group
                 if (threadIdx.x == 0) {
                     fence_proxy_async();
@@ -679,9 +703,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                 phase ^= 1;
                 resident = g;
             }
-            if (anyvalid == 0) continue;
-            const uint32_t *kl = reinterpret_cast<const uint32_t *>(s_tab);
-            const uint4 *recs = reinterpret_cast<const uint4 *>(s_tab + a.L.kl_bytes);
+            if (anyvalid != 0) {
+            const uint32_t *kl = reinterpret_cast<const uint32_t *>(tab);
+            const uint4 *recs = reinterpret_cast<const uint4 *>(tab + a.L.kl_bytes);
             const int np = group_size(g);
             const int n2 = a.nrec >> 1, n4 = a.nrec >> 2;
             for (int pl = slice; pl < np; pl += split) {
@@ -802,6 +826,25 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                 if constexpr (SPARSE)
                     if (compact) __syncwarp(); // the next couple rewrites s_list
             }
+            } // anyvalid
+            if (dbuf) {
+                // release the buffer; the last of the W warps (its (sq>>1)-th
+                // round of W arrivals completes) refills it with group sq + 2
+                __syncwarp();
+                if (lane == 0) {
+                    const int b = (int)(sq & 1);
+                    __threadfence_block();
+                    const uint32_t old = atomicAdd(&s_cnt[b], 1u);
+                    if (old == (uint32_t)(((sq >> 1) + 1) * W - 1) && sq + 2 < nseq) {
+                        const int gn = (int)((sq + 2) % a.groups);
+                        const uint32_t gb = group_blob(gn);
+                        fence_proxy_async();
+                        mbar_expect_tx(s_bar + b, gb);
+                        bulk_copy(s_tab + (size_t)b * a.L.group_bytes,
+                                  a.tables + (size_t)gn * a.L.group_bytes, gb, s_bar + b);
+                    }
+                }
+            }
         }
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
@@ -907,6 +950,12 @@ static int probe_smem_base(uint32_t *base)
     return FSP_OK;
 }
 
+static bool dbuf_on()
+{
+    const char *s = getenv("FSP_LB_DBUF");
+    return s ? atoi(s) != 0 : true;
+}
+
 // Choose the machine specialisation, warps per CTA and couple groups so that
 // one couple group + PTM + U + per-warp scratch fit the opt-in shared memory
 // and every U address fits the 16-bit record field.
@@ -994,7 +1043,7 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                 if (tm_cols > 512) continue;
             }
             L.rt_bytes = nib ? 0 : 3 * (size_t)pl.maxm * 32 * npl * (pl.s16 ? 2 : 4);
-            L.off_rt = L.off_bar + 16;
+            L.off_rt = L.off_bar + 32;
             L.list_bytes = pl.sparse ? align16(((size_t)pl.nrec + FSP_REC_SLACK + 4) * 8) : 0;
             L.off_list = align16(L.off_rt + (size_t)W * L.rt_bytes);
             L.off_tab = align16(L.off_list + (size_t)W * L.list_bytes);
@@ -1005,7 +1054,10 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                 // + FSP_REC_SLACK padding records for the walk's look-ahead
                 const size_t gb = align16(L.kl_bytes +
                                           ((size_t)ppg * pl.nrec + FSP_REC_SLACK) * sizeof(fsp_rec));
-                if (L.off_tab + gb <= (size_t)optin) {
+                // two or more groups: double-buffered (two group buffers) unless
+                // FSP_LB_DBUF=0 (one buffer, CTA barrier per group switch)
+                const bool db = Greal > 1 && dbuf_on();
+                if (L.off_tab + (db ? 2 : 1) * gb <= (size_t)optin) {
                     fsp_lb_plan c = pl;
                     L.group_bytes = gb;
                     c.L = L;
@@ -1013,14 +1065,15 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                     c.groups = Greal;
                     c.pairs_per_group = ppg;
                     c.warps = W;
-                    c.smem_bytes = L.off_tab + gb;
+                    c.smem_bytes = L.off_tab + (db ? 2 : 1) * gb;
+                    c.dbuf = db;
                     c.tm_cols = tm_cols;
                     // co-resident CTAs must fit the SM's 512 TMEM columns (an
                     // allocation beyond them would wait for another CTA to exit)
                     if (occupancy_of(c) == FSP_OK && c.ctas_per_sm > 0 &&
                         c.ctas_per_sm * tm_cols <= 512) {
                         const double score = (double)W * c.ctas_per_sm * (npl == 4 ? 1.5 : 1.0) /
-                                             (1.0 + 0.015 * (Greal - 1));
+                                             (1.0 + (db ? 0.005 : 0.015) * (Greal - 1));
                         if (score > best) {
                             best = score;
                             bestp = c;
@@ -1078,6 +1131,7 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.stride = stride;
     a.hi_mul = 0x10000u;
     a.tm_cols = (uint32_t)pl.tm_cols;
+    a.dbuf = pl.dbuf ? 1 : 0;
     // couple split for pools with fewer tiles than warp slots (latency-bound
     // otherwise: a 4,096-node pool is 32 tiles on 148 x 16 warps); the pool size
     // of a device-sized launch (B&B) is only bounded by `pool`
