@@ -51,6 +51,8 @@ static void build_tables(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl
         }
     }
     std::vector<int> order(n), A(n), B(n);
+    int D = 0; // 16-bit walk offset: max p (lb_kernel.cu upd<>)
+    for (int64_t i = 0; i < (int64_t)n * m; ++i) D = std::max(D, (int)ptm[i]);
     int p = 0;
     for (int k = 0; k < m; ++k) {
         for (int l = k + 1; l < m; ++l, ++p) {
@@ -75,9 +77,9 @@ static void build_tables(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl
             for (int i = 0; i < n; ++i) {
                 const int j = order[i];
                 const int x = ptm[(size_t)j * m + l] - ptm[(size_t)j * m + k];
-                // s16 walk: y < 2^15 in the low half, the job id in the high
-                // half (read by the sparse walk's compaction only)
-                rec[i].c1 = pl.s16 ? (int32_t)(((uint32_t)j << 16) | (uint32_t)B[j]) : B[j];
+                // 16-bit walk: y + D < 2^16 in the low half, the job id in the
+                // high half (read by the sparse walk's compaction only)
+                rec[i].c1 = pl.s16 ? (int32_t)(((uint32_t)j << 16) | (uint32_t)(B[j] + D)) : B[j];
                 rec[i].meta = pl.s16 ? (int32_t)((uaddr(j) << 16) | ((uint32_t)x & 0xffffu))
                                      : (int32_t)(((uint32_t)x << 16) | uaddr(j));
             }

@@ -166,6 +166,7 @@ struct LbArgs {
     int vec_rows;          // vectorised scheduled-set build (long prefixes)
     uint32_t tm_cols;      // TMEM columns allocated per CTA (TM variants)
     int dbuf;              // couple groups double-buffered (groups >= 2): no CTA barrier
+    int woff;              // 16-bit walk offset D (= max p): e + D is carried
     int split;             // warps per tile (power of two <= W): each walks every
                            // split-th couple, LBs combined by atomicMax (lb_out zeroed)
 };
@@ -239,16 +240,19 @@ __device__ __forceinline__ Mask<NPL> lds_mask(uint32_t addr)
 // is  e = max(e + x_j, y_j)  with x_j = p_jl - p_jk, y_j = lag_j + p_jl.  Line 10
 // ("job not yet scheduled") is the predicate (a short branch ptxas predicates).
 //   int32: e = max(e + x, y)  (x = top half of meta, extracted once per position)
-//   s16:   the low halfword carries e (0 <= e <= t2 fits int16, host-checked):
-//          e = max.s16(e + meta, c1) (VIADDMNMX.S16x2; the low halves are x and
-//          y, the high halves only collect garbage that never reaches the low one)
+//   16-bit: the low halfword carries e + D, D = max p (the walk offset):
+//          0 <= e <= t2 <= (n+m-1)*max p and e + x >= 0 with x >= -max p, so
+//          e + D and e + D + x stay in [0, 65535] (host-checked) and
+//          e + D = max.u16(e + D + meta, c1) (VIADDMNMX.U16x2; the low halves
+//          are x and y + D, the high halves only collect garbage that never
+//          reaches the low one)
 template <bool S16>
 __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1, uint32_t x,
                                     int &e)
 {
     if (bits & lanebit) {
         asm volatile(""); // keep the branch so ptxas predicates the op
-        if constexpr (S16) e = (int)__viaddmax_s16x2((unsigned)e, x, c1);
+        if constexpr (S16) e = (int)__viaddmax_u16x2((unsigned)e, x, c1);
         else e = __viaddmax_s32(e, (int)x, (int)c1);
     }
 }
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     // per-warp heads R[MAXM][TN], A = R + L [MAXM][TN] (L_k = sum of p_jk over
     // the unscheduled jobs) and tails Q[MAXM][TN]; int16 in the s16 walk (all
     // values fit, host-checked), int32 otherwise
-    using rt_t = typename std::conditional<S16, int16_t, int32_t>::type;
+    using rt_t = typename std::conditional<S16, uint16_t, int32_t>::type;
     rt_t *Rs = reinterpret_cast<rt_t *>(smem + a.L.off_rt + (size_t)warp * a.L.rt_bytes);
     rt_t *As = Rs + MAXM * TN;
     rt_t *Qs = As + MAXM * TN;
@@ -341,6 +345,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     // group sequence number sq lives in buffer sq & 1, whose (sq >> 1)-th fill
     // it is; the last warp to release a buffer refills it with group sq + 2
     const bool dbuf = a.dbuf != 0;
+    const int woff = S16 ? a.woff : 0;
     const long long nseq = niter * a.groups;
 
     // ---- stage PTM + the first couple group(s) (TMA bulk, mbarriers) ----
@@ -720,11 +725,11 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                     tm_ld<NPLP>(tbase + (0 * HM + (k >> 1)) * NPLP, rk);
                     tm_wait_ld<NPLP>(rl, rk);
 #pragma unroll
-                    for (int q = 0; q < NPL; ++q) ee[q] = tm_half(rl[q], l & 1) - tm_half(rk[q], k & 1);
+                    for (int q = 0; q < NPL; ++q) ee[q] = tm_half(rl[q], l & 1) - tm_half(rk[q], k & 1) + woff;
                 } else {
 #pragma unroll
                     for (int q = 0; q < NPL; ++q)
-                        ee[q] = (int)Rs[l * TN + q * 32 + lane] - (int)Rs[k * TN + q * 32 + lane];
+                        ee[q] = (int)Rs[l * TN + q * 32 + lane] - (int)Rs[k * TN + q * 32 + lane] + woff;
                 }
                 const uint4 *rp = recs + (size_t)pl * n2;
                 int n4c = n4;
@@ -807,7 +812,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
                 }
                 if constexpr (S16) {
 #pragma unroll
-                    for (int q = 0; q < NPL; ++q) ee[q] = (int)(int16_t)(ee[q] & 0xffff);
+                    for (int q = 0; q < NPL; ++q) ee[q] = (int)(ee[q] & 0xffff) - woff;
                 }
                 // lines 18-19: timeOnM2 = t1 + e with t1 = R_k + L_k at the end
                 if constexpr (TM) {
@@ -964,9 +969,9 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     fsp_lb_plan &pl = sparse ? inst->plan_bb : inst->plan;
     const int n = inst->n, m = inst->m, P = inst->P;
     pl.exact = (m == 5 || m == 10 || m == 20);
-    // 16-bit walk when every walk value fits int16: 0 <= e <= t2 <= (n+m-1)*max p,
-    // e + x >= -max p, and R, A, Q are bounded by t2
-    pl.s16 = (int64_t)(n + m - 1) * inst->max_p <= 32767;
+    // 16-bit walk when e + D fits u16 with D = max p: 0 <= e <= t2 <= (n+m-1)*max p,
+    // e + x >= -max p; R, A, Q are bounded by t2
+    pl.s16 = (int64_t)(n + m) * inst->max_p <= 65535;
     if (const char *s = getenv("FSP_LB_S16")) pl.s16 = pl.s16 && atoi(s) != 0;
     // sparse walk: exact-m s16 specialisations (records carry the job id),
     // 64 <= n <= 1024 (below 64 jobs the compaction does not pay: measured)
@@ -1132,6 +1137,7 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.hi_mul = 0x10000u;
     a.tm_cols = (uint32_t)pl.tm_cols;
     a.dbuf = pl.dbuf ? 1 : 0;
+    a.woff = inst->max_p;
     // couple split for pools with fewer tiles than warp slots (latency-bound
     // otherwise: a 4,096-node pool is 32 tiles on 148 x 16 warps); the pool size
     // of a device-sized launch (B&B) is only bounded by `pool`
