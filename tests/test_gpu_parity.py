@@ -232,3 +232,20 @@ def test_parity_couple_split(torch, fsp, orc, monkeypatch, split):
     ptm = inputs.taillard(n, m, seed)
     pf, dp = inputs.pool_d1(n, 3001, inputs.pool_seed("ta021") + 77)
     compare(torch, fsp, orc, ptm, pf, dp)
+
+
+@pytest.mark.parametrize("n,m", [(20, 5), (20, 20), (70, 10)])
+def test_parity_walk16_offset_boundary(torch, fsp, orc, n, m):
+    """The 16-bit walk carries e + max p unsigned and is taken iff
+    (n + m) * max p <= 65535: instances exactly at the largest
+    admissible max p (16-bit walk, every value up to its limit) and one above it
+    (int32 walk) both match the oracle bit for bit."""
+    pmax16 = 65535 // (n + m)
+    for pmax, walk16 in [(pmax16, 1), (pmax16 + 1, 0)]:
+        rng = np.random.default_rng(1208 + n * m + pmax)
+        ptm = rng.integers(pmax // 2, pmax + 1, size=(n, m)).astype(np.int32)
+        ptm[rng.integers(n), rng.integers(m)] = pmax
+        ptm[0, :] = pmax  # one job at max p on every machine: t2 near its bound
+        pf, dp = inputs.pool_d1(n, 3000, 4242 + pmax)
+        inst = compare(torch, fsp, orc, ptm, pf, dp)
+        assert inst.info["walk16"] == walk16
