@@ -54,6 +54,7 @@ struct fsp_lb_plan {
     int groups;          // couple groups (one resident in smem at a time)
     int pairs_per_group; // couples per group (last group may be shorter)
     bool dbuf;           // groups >= 2 double-buffered in shared memory
+    bool byte_rows;      // 16-bit walk, m >= 10: U rows of one byte per lane (else nibbles)
     int warps;           // warps per CTA
     int ctas_per_sm;
     int num_sms;

@@ -189,27 +189,32 @@ __device__ __forceinline__ uint32_t mask_addr(uint32_t meta, uint32_t wst, uint3
 
 // U row layouts (one row per job, one segment per warp):
 //  * lane-major (int32 walk): NPL words, bit L of word q = node q*32+L;
-//  * nibble (s16 walk): lane L owns NPL+1 consecutive bits of word L/LPW at
-//    shift 1 + (L % LPW)*(NPL+1); bit 1+q of the field = node q*32+L (bit 0 of
-//    the field and bit 0 of the word stay clear, so every lane's shift is >= 1
-//    and can be a multiply-high).  A lane loads one word, shifts once, and R2P
-//    turns its NPL bits into the predicates P1..P4 of the updates (instead of
-//    one LOP3 per node: the ALU pipe is the walk's bottleneck).
-template <int NPL>
+//  * byte (16-bit walk, m >= 10, BYTE): lane L owns byte L of the warp's
+//    8-word row segment; bit 1+q of the byte = node q*32+L.  A lane loads its
+//    byte (LDS.U8, zero-extended: no shift) and R2P turns bits 1..NPL into the
+//    predicates P1..P4 of the updates (instead of one LOP3 per node);
+//  * nibble (16-bit walk, m >= 10, !BYTE: long job lists, where 32 bytes per
+//    row and warp do not fit): lane L owns NPL+1 bits of word L/LPW at shift
+//    1 + (L % LPW)*(NPL+1); bit 1+q of the field = node q*32+L.  A lane loads
+//    one word and shifts it by a multiply-high (FMA pipe) before the R2P.
+template <int NPL, bool BYTE>
 struct Nib {
-    static constexpr int FO = 2;                              // first node bit of lane 0
-    static constexpr int LPW = (32 - FO + 1) / (NPL + 1);     // lanes per word
+    static constexpr int LPW = BYTE ? 4 : 31 / (NPL + 1);    // lanes per word
     static constexpr int WPR = (32 + LPW - 1) / LPW;          // words per warp segment
 };
 
-template <bool S16, int NPL, int MAXM>
+template <bool S16, int NPL, int MAXM, bool BYTE>
 struct ULayout {
-    // nibble rows where the couple walk dominates (m >= 10); lane-major rows for
-    // m = 5, where the per-node phase dominates (measured on 20x5)
+    // byte / nibble rows where the couple walk dominates (m >= 10); lane-major
+    // rows for m = 5, where the per-node phase dominates (measured on 20x5)
     static constexpr bool NIB = S16 && MAXM >= 10;
-    static constexpr int WPR = NIB ? Nib<NPL>::WPR : NPL;
-    __device__ static int word(int L, int q) { return NIB ? L / Nib<NPL>::LPW : q; }
-    __device__ static int bit(int L, int q) { return NIB ? (L % Nib<NPL>::LPW) * (NPL + 1) + Nib<NPL>::FO + q : L; }
+    static constexpr bool BYTES = NIB && BYTE;
+    static constexpr int WPR = NIB ? Nib<NPL, BYTE>::WPR : NPL;
+    __device__ static int word(int L, int q) { return NIB ? L / Nib<NPL, BYTE>::LPW : q; }
+    __device__ static int bit(int L, int q)
+    {
+        return !NIB ? L : BYTE ? (L % 4) * 8 + 1 + q : (L % Nib<NPL, BYTE>::LPW) * (NPL + 1) + 2 + q;
+    }
 };
 
 // The NPL unscheduled-bit words of one job for this warp's NPL*32 nodes.
@@ -218,11 +223,14 @@ struct Mask {
     uint32_t b[NPL];
 };
 
-template <int NPL>
+template <int NPL, bool BYTE = false>
 __device__ __forceinline__ Mask<NPL> lds_mask(uint32_t addr)
 {
     Mask<NPL> v;
-    if constexpr (NPL == 1) {
+    if constexpr (BYTE) {
+        static_assert(NPL == 1, "one byte per lane");
+        asm("ld.shared.u8 %0, [%1];" : "=r"(v.b[0]) : "r"(addr));
+    } else if constexpr (NPL == 1) {
         asm("ld.shared.u32 %0, [%1];" : "=r"(v.b[0]) : "r"(addr));
     } else if constexpr (NPL == 2) {
         asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.b[0]), "=r"(v.b[1]) : "r"(addr));
@@ -258,12 +266,13 @@ __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1
 }
 
 // nibble layout: one word per lane (MW = 1); lane-major: NPL words
-#define FSP_MASK(META) lds_mask<MW>(mask_addr<S16>((META), wst, hi_mul, wst64))
+#define FSP_MASK(META) lds_mask<MW, UL::BYTES>(mask_addr<S16>((META), wst, hi_mul, wst64))
 #define FSP_UPD(MASK, C1, META)                                                 \
     {                                                                           \
         const uint32_t x_ = S16 ? (META) : (uint32_t)((int)(META) >> 16);       \
         if constexpr (UL::NIB) {                                                \
-            const uint32_t nb_ = __umulhi((MASK).b[0], shmul);                  \
+            /* byte rows: the lane's byte; nibble rows: shifted by a mul-hi */  \
+            const uint32_t nb_ = UL::BYTES ? (MASK).b[0] : __umulhi((MASK).b[0], shmul); \
             _Pragma("unroll") for (int q_ = 0; q_ < NPL; ++q_)                  \
                 upd<S16>(nb_, 2u << q_, (C1), x_, ee[q_]);                      \
         } else {                                                                \
@@ -272,8 +281,12 @@ __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1
         }                                                                       \
     }
 
-template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE>
-__global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbArgs a)
+// launch bounds: 8 warps for m > 20; 4 warps x 5 CTAs per SM for m = 5 (the
+// per-node phase dominates there: small CTAs, registers capped at 96 so five
+// fit; measured 20x5: 5.0 G bounds/s vs 3.9 G with one 16-warp CTA); else 16
+template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE, bool BYTE = true>
+__global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM <= 5 ? 5 : 1)
+    lb_kernel(const LbArgs a)
 {
     extern __shared__ __align__(128) uint8_t smem[];
     const int n = a.n;
@@ -285,7 +298,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     // nibble layout, one block per warp [W][(n+1)][urow] (records hold the row
     // offset, the warp's block base is added per visit: no 64 KB limit on W)
     uint32_t *Uw = reinterpret_cast<uint32_t *>(smem + a.L.off_u) +
-                   (ULayout<S16, NPL, MAXM>::NIB ? (size_t)warp * (n + 1) * a.L.urow_words : 0);
+                   (ULayout<S16, NPL, MAXM, BYTE>::NIB ? (size_t)warp * (n + 1) * a.L.urow_words : 0);
     const int32_t *s_ptm = reinterpret_cast<const int32_t *>(smem + a.L.off_ptm);
     // TM variants: per job [p pairs x HMP][q pairs x HMP] u32 after PTM (see fsp_plan_lb)
     const uint32_t *s_pq = reinterpret_cast<const uint32_t *>(s_ptm + (size_t)a.n * a.mp4);
@@ -309,7 +322,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     // TM: the per-node R, A, Q of phase A go to tensor memory, two machines per
     // 32-bit column (16-bit values): column (arr*HM + k/2)*NPL + q of this
     // warp's block in its lane quarter (warp % 4), blocks of TCOLS columns
-    constexpr bool TM = ULayout<S16, NPL, MAXM>::NIB;
+    constexpr bool TM = ULayout<S16, NPL, MAXM, BYTE>::NIB;
     constexpr int NPLP = NPL; // TMEM columns per (array, machine pair)
     constexpr int HM = (MAXM + 1) / 2, TCOLS = 3 * HM * NPLP;
     constexpr int HMP = (HM + 3) & ~3; // machine pairs per packed row, padded to 16 bytes
@@ -378,16 +391,17 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : 512, 1) lb_kernel(const LbAr
     // tiles of a partial last iteration spread over every SM (a few idle warps
     // per CTA) instead of leaving whole SMs idle
     const uint32_t lanebit = 1u << lane;
-    using UL = ULayout<S16, NPL, MAXM>;
+    using UL = ULayout<S16, NPL, MAXM, BYTE>;
     constexpr int WPR = UL::WPR;                 // U words per warp per job row
     constexpr int MW = UL::NIB ? 1 : NPL;        // mask words a lane loads
     const int lw = UL::word(lane, 0);            // nibble layout: this lane's word
-    const int lsh = UL::NIB ? UL::bit(lane, 0) - 1 : 0; // ... and bit offset
-    // nibble layout: the shift (lsh >= 1) that brings this lane's NPL bits to
-    // bits 1..NPL (R2P -> P1..P4), done as a multiply-high by 2^(32 - lsh) on the
-    // FMA pipe (the ALU pipe, which runs the updates, is the walk's bottleneck)
-    const uint32_t shmul = UL::NIB ? 1u << (32 - lsh) : 1u;
-    const uint32_t wst = UL::NIB ? smem_u32(Uw) + 4u * lw : 4u * (WPR * warp);
+    // byte rows: the lane's mask byte is at byte offset `lane` of the row
+    // segment; nibble rows: the lane's word, shifted (lsh >= 1) to bits 1..NPL by
+    // a multiply-high by 2^(32 - lsh) on the FMA pipe
+    const int lsh = (UL::NIB && !UL::BYTES) ? UL::bit(lane, 0) - 1 : 1;
+    const uint32_t shmul = 1u << (32 - lsh);
+    const uint32_t wst = UL::BYTES ? smem_u32(Uw) + (uint32_t)lane
+                         : UL::NIB ? smem_u32(Uw) + 4u * lw : 4u * (WPR * warp);
     const int urow = a.L.urow_words; // words per job row of U (padded against bank conflicts)
     const uint32_t hi_mul = a.hi_mul;
     const uint64_t wst64 = (uint64_t)wst << 32;
@@ -875,25 +889,25 @@ __global__ void smem_base_probe(uint32_t *out)
     *out = smem_u32(smem);
 }
 
-template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE>
+template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE, bool BYTE = true>
 int launch(const fsp_lb_plan &pl, const LbArgs &a, cudaStream_t s)
 {
-    lb_kernel<MAXM, EXACT, S16, NPL, SPARSE><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
+    lb_kernel<MAXM, EXACT, S16, NPL, SPARSE, BYTE><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, "lb_kernel launch");
 }
 
-template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE>
+template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE, bool BYTE = true>
 int configure(fsp_lb_plan &pl)
 {
     // the attribute is per kernel variant and shared by every instance: set it
     // to the device's opt-in maximum, never to this plan's size
-    cudaError_t e = cudaFuncSetAttribute(lb_kernel<MAXM, EXACT, S16, NPL, SPARSE>,
+    cudaError_t e = cudaFuncSetAttribute(lb_kernel<MAXM, EXACT, S16, NPL, SPARSE, BYTE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          pl.smem_optin);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "cudaFuncSetAttribute");
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM, EXACT, S16, NPL, SPARSE>,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM, EXACT, S16, NPL, SPARSE, BYTE>,
                                                       pl.warps * 32, pl.smem_bytes);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "occupancy");
     if (per_sm < 1) return fsp_fail(FSP_ERANGE, "lb kernel does not fit on an SM");
@@ -910,6 +924,9 @@ int configure(fsp_lb_plan &pl)
         if (pl.sparse)                                                          \
             return pl.npl == 4 ? FN<M, true, S, 4, true>(__VA_ARGS__)           \
                                : FN<M, true, S, 2, true>(__VA_ARGS__);          \
+        if (!pl.byte_rows)                                                      \
+            return pl.npl == 4 ? FN<M, true, S, 4, false, false>(__VA_ARGS__)   \
+                               : FN<M, true, S, 2, false, false>(__VA_ARGS__);  \
         return pl.npl == 4 ? FN<M, true, S, 4, false>(__VA_ARGS__)              \
                            : FN<M, true, S, 2, false>(__VA_ARGS__);
 #define FSP_DISPATCH_M(FN, S, ...)                                              \
@@ -1005,12 +1022,16 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     // TMEM heads (ta091 B&B: 390 M nodes/s vs 314 M with 64-node blocks, whose
     // smaller live sets no longer outweigh the per-node table and mask traffic)
     if (pl.sparse) npl_lo = npl_hi = getenv("FSP_BB_NPL") && atoi(getenv("FSP_BB_NPL")) == 2 ? 2 : 4;
-    int w_lo = 1, w_hi = pl.maxm > 20 ? 8 : 16; // launch bounds of the wide variants
+    int w_lo = 1, w_hi = pl.maxm > 20 ? 8 : pl.maxm <= 5 ? 4 : 16; // = the kernel's launch bounds
     if (const char *s = getenv("FSP_LB_WARPS")) w_lo = w_hi = std::max(1, std::min(w_hi, atoi(s)));
     double best = -1.0;
     fsp_lb_plan bestp = pl;
     for (int npl = npl_lo; npl <= npl_hi; npl += 2) {
+        for (int lay = 0; lay < 2; ++lay) // 0: byte rows, 1: nibble rows (m >= 10, not sparse)
         for (int W = w_hi; W >= w_lo; --W) {
+            if (lay == 1 && !(pl.s16 && pl.maxm >= 10 && pl.exact && !pl.sparse)) break;
+            if (const char *e = getenv("FSP_LB_ROWS")) // experiments: 0 = byte, 1 = nibble
+                if (atoi(e) != lay && pl.s16 && pl.maxm >= 10 && pl.exact && !pl.sparse) break;
             // warps are dealt to the 4 SMSPs by id % 4: a W that is not a multiple
             // of 4 leaves some SMSPs with an extra warp that paces the whole CTA
             // (measured: 200x20, 10 warps 120 M/s vs 12 warps 140 M/s)
@@ -1024,7 +1045,9 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
             // s16: nibble rows (one word per lane, ceil(32/LPW) words per warp);
             // made odd so the 32 jobs a warp clears at once hit 32 banks
             const bool nib = pl.s16 && pl.maxm >= 10; // = ULayout::NIB
-            const int lpw = 31 / (npl + 1), wpr = nib ? (32 + lpw - 1) / lpw : npl; // = Nib<npl>
+            // = ULayout::WPR: byte rows 8 words (32 lanes x 8 bits), nibble rows
+            // ceil(32 / lanes per word)
+            const int wpr = !nib ? npl : lay == 0 ? 8 : (32 + 31 / (npl + 1) - 1) / (31 / (npl + 1));
             // nibble: per-warp blocks of (n+1) rows of wpr|1 words (odd: the 32 jobs a
             // warp clears at once hit 32 banks); record offsets j*4*urow < 64 KB
             const int urow = nib ? wpr | 1 : npl * W;
@@ -1073,11 +1096,14 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                     c.smem_bytes = L.off_tab + (db ? 2 : 1) * gb;
                     c.dbuf = db;
                     c.tm_cols = tm_cols;
+                    c.byte_rows = lay == 0;
                     // co-resident CTAs must fit the SM's 512 TMEM columns (an
                     // allocation beyond them would wait for another CTA to exit)
                     if (occupancy_of(c) == FSP_OK && c.ctas_per_sm > 0 &&
                         c.ctas_per_sm * tm_cols <= 512) {
-                        const double score = (double)W * c.ctas_per_sm * (npl == 4 ? 1.5 : 1.0) /
+                        // byte rows: one FMA op less per position (+11 % at 200x20)
+                        const double score = (double)W * c.ctas_per_sm * (npl == 4 ? 1.5 : 1.0) *
+                                             (nib && lay == 0 ? 1.1 : 1.0) /
                                              (1.0 + (db ? 0.005 : 0.015) * (Greal - 1));
                         if (score > best) {
                             best = score;
