@@ -605,14 +605,8 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 L2[kp] = 0;
             }
             int cnt = 0;
-            for (int j = 0; j < n; ++j) {
-                const uint32_t uj = Uw[j * urow + useg + UL::word(lane, q)];
-                const bool act = (uj >> UL::bit(lane, q)) & 1u;
-                if constexpr (UL::NIB) {
-                    if (!__any_sync(0xffffffffu, act)) continue; // scheduled everywhere
-                } else {
-                    if (uj == 0) continue; // scheduled in every node of this half-warp
-                }
+            // a2/a3 for job j if it is unscheduled in this lane's node q
+            auto visit = [&](int j, bool act) {
                 if (act) {
                     ++cnt;
                     const int4 *pr = reinterpret_cast<const int4 *>(s_ptm + j * a.mp4);
@@ -673,6 +667,30 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                             }
                         }
                     }
+                }
+            };
+            if constexpr (SPARSE) {
+                // only the warp's live jobs (unscheduled in some node of the
+                // warp): deep B&B blocks have a few dozen of n
+                for (int w0 = 0; w0 * 32 < n; ++w0) {
+                    uint32_t bits = __shfl_sync(0xffffffffu, livew, w0);
+                    while (bits) {
+                        const int j = w0 * 32 + __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        const uint32_t uj = Uw[j * urow + useg + UL::word(lane, q)];
+                        visit(j, (uj >> UL::bit(lane, q)) & 1u);
+                    }
+                }
+            } else {
+                for (int j = 0; j < n; ++j) {
+                    const uint32_t uj = Uw[j * urow + useg + UL::word(lane, q)];
+                    const bool act = (uj >> UL::bit(lane, q)) & 1u;
+                    if constexpr (UL::NIB) {
+                        if (!__any_sync(0xffffffffu, act)) continue; // scheduled everywhere
+                    } else {
+                        if (uj == 0) continue; // scheduled in every node of this half-warp
+                    }
+                    visit(j, act);
                 }
             }
             if (node < pool && cnt != n - d) bad = true; // repeated / bad job
