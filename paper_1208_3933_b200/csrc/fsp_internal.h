@@ -40,6 +40,8 @@ struct fsp_lb_layout {
     size_t off_list, list_bytes; // per warp (sparse walk): compacted records of a couple
     size_t off_tab;            // one couple group: [kl header][records]
     size_t kl_bytes, group_bytes;
+    size_t pos_off;            // sparse plans, n <= 256: offset of the inverse position
+                               //   table u8 [couple][job] in a group (0: none)
 };
 
 struct fsp_lb_plan {

@@ -74,6 +74,8 @@ static void build_tables(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl
                 return x < y;
             });
             fsp_rec *rec = reinterpret_cast<fsp_rec *>(gb + kl_bytes) + (size_t)pl_idx * pl.nrec;
+            if (pl.L.pos_off) // inverse position table: pos[couple][job]
+                for (int i = 0; i < n; ++i) gb[pl.L.pos_off + (size_t)pl_idx * n + order[i]] = (uint8_t)i;
             for (int i = 0; i < n; ++i) {
                 const int j = order[i];
                 const int x = ptm[(size_t)j * m + l] - ptm[(size_t)j * m + k];

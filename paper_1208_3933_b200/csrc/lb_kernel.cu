@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
         return np < a.ppg ? np : a.ppg;
     };
     auto group_blob = [&](int g) {
+        if (a.L.pos_off) return (uint32_t)a.L.group_bytes; // + the inverse position table
         return (uint32_t)((a.L.kl_bytes +
                            ((size_t)group_size(g) * a.nrec + FSP_REC_SLACK) * sizeof(fsp_rec) + 15) &
                           ~size_t(15));
@@ -522,6 +523,21 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             }
         }
         const bool compact = SPARSE && live + 16 <= n;
+        // few live jobs (deep B&B blocks): compaction by the inverse position
+        // table (plan with pos_off), lane t < live holding the t-th live job
+        const bool inv = SPARSE && compact && live <= 32 && a.L.pos_off != 0;
+        int jt = 0;
+        if constexpr (SPARSE) {
+            if (inv) {
+                int base = 0;
+                for (int w0 = 0; w0 * 32 < n; ++w0) {
+                    const uint32_t bits = __shfl_sync(0xffffffffu, livew, w0);
+                    const int c = __popc(bits);
+                    if (lane >= base && lane < base + c) jt = w0 * 32 + (int)__fns(bits, 0, lane - base + 1);
+                    base += c;
+                }
+            }
+        }
 
         // ---------------- per node of this lane: C, heads, tails ----------------
 #pragma unroll 1
@@ -794,6 +810,17 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                         // depend on the running count
                         int cnt = 0;
                         const uint32_t lt = (1u << lane) - 1u;
+                        if (inv) {
+                            // <= 32 live jobs: lane t takes live job jt, reads its
+                            // position in this couple's JM order from the inverse
+                            // table, ranks it among the live positions (live-count
+                            // shuffles) and stores its record at that rank
+                            const int key = lane < live ? (int)(tab + a.L.pos_off)[pl * n + jt] : 0x7fffffff;
+                            int rank = 0;
+                            for (int u = 0; u < live; ++u) rank += __shfl_sync(0xffffffffu, key, u) < key;
+                            if (lane < live) s_list[rank] = col[key];
+                            cnt = live;
+                        } else
                         for (int i0 = 0; i0 < a.nrec; i0 += 128) {
                             uint2 r[4];
                             uint32_t bal[4];
@@ -1118,8 +1145,15 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                 const int Greal = (P + ppg - 1) / ppg;
                 L.kl_bytes = align16((size_t)ppg * 4);
                 // + FSP_REC_SLACK padding records for the walk's look-ahead
-                const size_t gb = align16(L.kl_bytes +
-                                          ((size_t)ppg * pl.nrec + FSP_REC_SLACK) * sizeof(fsp_rec));
+                size_t gb = align16(L.kl_bytes +
+                                    ((size_t)ppg * pl.nrec + FSP_REC_SLACK) * sizeof(fsp_rec));
+                // sparse plan, n <= 256: + the inverse position table (u8
+                // [couple][job] = position of the job in the couple's JM order)
+                L.pos_off = 0;
+                if (pl.sparse && n <= 256 && !getenv("FSP_BB_NOINV")) {
+                    L.pos_off = gb;
+                    gb = align16(gb + (size_t)ppg * n);
+                }
                 // two or more groups: double-buffered (two group buffers) unless
                 // FSP_LB_DBUF=0 (one buffer, CTA barrier per group switch)
                 const bool db = Greal > 1 && dbuf_on();
