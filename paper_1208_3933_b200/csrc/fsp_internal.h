@@ -17,6 +17,8 @@
 // DESIGN.md §6 derives the one-update form e <- max(e + x, y) of Fig. 3 lines 11-15.
 // Padding records after the last couple of a group (walk look-ahead).
 #define FSP_REC_SLACK 8
+// most couple-group buffers per CTA (multi-buffered groups)
+#define FSP_MAX_GBUF 4
 
 struct __align__(8) fsp_rec {
     int32_t c1;
@@ -35,7 +37,7 @@ struct fsp_lb_layout {
                                //   layout: one [(n+1)][urow_words] block per warp):
     int urow_words;            //   word warp*npl + q of job j's row = nodes q*32..q*32+31
     size_t off_ptm, ptm_bytes; // PTM int32 [n][mp4]
-    size_t off_bar;            // mbarriers, buffer release counters, TMEM address (32 B)
+    size_t off_bar;            // mbarriers, buffer release counters, TMEM address (16 B x FSP_MAX_GBUF)
     size_t off_rt, rt_bytes;   // per warp: R, A (= R + L), Q, each [MAXM][32*npl]
     size_t off_list, list_bytes; // per warp (sparse walk): compacted records of a couple
     size_t off_tab;            // one couple group: [kl header][records]
@@ -55,7 +57,7 @@ struct fsp_lb_plan {
     fsp_lb_layout L;
     int groups;          // couple groups (one resident in smem at a time)
     int pairs_per_group; // couples per group (last group may be shorter)
-    bool dbuf;           // groups >= 2 double-buffered in shared memory
+    int dbuf;            // couple-group buffers in shared memory (0: one + CTA barrier)
     bool byte_rows;      // 16-bit walk, m >= 10: U rows of one byte per lane (else nibbles)
     int warps;           // warps per CTA
     int ctas_per_sm;

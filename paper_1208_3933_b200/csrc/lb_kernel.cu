@@ -167,7 +167,7 @@ struct LbArgs {
     int cin_stride;
     int vec_rows;          // vectorised scheduled-set build (long prefixes)
     uint32_t tm_cols;      // TMEM columns allocated per CTA (TM variants)
-    int dbuf;              // couple groups double-buffered (groups >= 2): no CTA barrier
+    int dbuf;              // couple-group buffers (>= 2: multi-buffered, no CTA barrier)
     int woff;              // 16-bit walk offset D (= max p): e + D is carried
     int split;             // warps per tile (power of two <= W): each walks every
                            // split-th couple, LBs combined by atomicMax (lb_out zeroed)
@@ -331,8 +331,8 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
     // barrier area (32 B): [0] mbarrier "group buffer 0 full" (with PTM), [1]
     // "buffer 1 full", [2] release counters of the two buffers (u32 x 2), [3] TMEM
     // base address
-    uint32_t *s_cnt = reinterpret_cast<uint32_t *>(s_bar + 2);
-    uint32_t *s_tm = reinterpret_cast<uint32_t *>(s_bar + 3);
+    uint32_t *s_cnt = reinterpret_cast<uint32_t *>(s_bar + FSP_MAX_GBUF);
+    uint32_t *s_tm = s_cnt + FSP_MAX_GBUF;
     if constexpr (TM) {
         if (warp == 0) tm_alloc(s_tm, a.tm_cols);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -358,25 +358,30 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
     const int Wt = W / split; // tiles per CTA iteration
     const long long niter = (ntiles + (long long)Wt * gridDim.x - 1) / ((long long)Wt * gridDim.x);
     // double-buffered couple groups: the CTA's sequence of groups is it*G + gi;
-    // group sequence number sq lives in buffer sq & 1, whose (sq >> 1)-th fill
-    // it is; the last warp to release a buffer refills it with group sq + 2
-    const bool dbuf = a.dbuf != 0;
+    // group sequence number sq lives in buffer sq % NB, whose (sq / NB)-th fill
+    // it is; the last warp to release a buffer refills it with group sq + NB
+    // (a warp runs at most NB - 1 groups ahead of the slowest of its CTA)
+    const int NB = a.dbuf;
+    const bool dbuf = NB >= 2;
     const int woff = S16 ? a.woff : 0;
     const long long nseq = niter * a.groups;
 
     // ---- stage PTM + the first couple group(s) (TMA bulk, mbarriers) ----
     if (threadIdx.x == 0) {
-        mbar_init(s_bar, 1);
-        mbar_init(s_bar + 1, 1);
-        s_cnt[0] = s_cnt[1] = 0;
+        for (int b = 0; b < FSP_MAX_GBUF; ++b) {
+            mbar_init(s_bar + b, 1);
+            s_cnt[b] = 0;
+        }
         uint32_t gb = group_blob(0);
         mbar_expect_tx(s_bar, gb + (uint32_t)a.L.ptm_bytes);
         bulk_copy(s_tab, a.tables, gb, s_bar);
         bulk_copy(smem + a.L.off_ptm, a.ptm, (uint32_t)a.L.ptm_bytes, s_bar);
-        if (dbuf && nseq >= 2) {
-            gb = group_blob(1);
-            mbar_expect_tx(s_bar + 1, gb);
-            bulk_copy(s_tab + a.L.group_bytes, a.tables + a.L.group_bytes, gb, s_bar + 1);
+        for (int b = 1; dbuf && b < NB && b < nseq; ++b) {
+            const int g = b % a.groups;
+            gb = group_blob(g);
+            mbar_expect_tx(s_bar + b, gb);
+            bulk_copy(s_tab + (size_t)b * a.L.group_bytes, a.tables + (size_t)g * a.L.group_bytes, gb,
+                      s_bar + b);
         }
     }
     __syncthreads();
@@ -761,8 +766,8 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             const long long sq = it * a.groups + gi;
             const uint8_t *tab = s_tab;
             if (dbuf) { // wait for this group's buffer; no CTA-wide barrier
-                const int b = (int)(sq & 1);
-                mbar_wait(s_bar + b, (uint32_t)((sq >> 1) & 1));
+                const int b = (int)(sq % NB);
+                mbar_wait(s_bar + b, (uint32_t)((sq / NB) & 1));
                 tab = s_tab + (size_t)b * a.L.group_bytes;
             } else if (g != resident) {
                 __syncthreads(); // every warp is done with the resident group
@@ -916,11 +921,11 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 // round of W arrivals completes) refills it with group sq + 2
                 __syncwarp();
                 if (lane == 0) {
-                    const int b = (int)(sq & 1);
+                    const int b = (int)(sq % NB);
                     __threadfence_block();
                     const uint32_t old = atomicAdd(&s_cnt[b], 1u);
-                    if (old == (uint32_t)(((sq >> 1) + 1) * W - 1) && sq + 2 < nseq) {
-                        const int gn = (int)((sq + 2) % a.groups);
+                    if (old == (uint32_t)((sq / NB + 1) * W - 1) && sq + NB < nseq) {
+                        const int gn = (int)((sq + NB) % a.groups);
                         const uint32_t gb = group_blob(gn);
                         fence_proxy_async();
                         mbar_expect_tx(s_bar + b, gb);
@@ -1037,10 +1042,13 @@ static int probe_smem_base(uint32_t *base)
     return FSP_OK;
 }
 
-static bool dbuf_on()
+// couple-group buffers per CTA when the couples take several groups
+// (FSP_LB_DBUF: 0/1 = one buffer + CTA barrier, 2..FSP_MAX_GBUF = multi-buffered)
+static int nbuf_want()
 {
     const char *s = getenv("FSP_LB_DBUF");
-    return s ? atoi(s) != 0 : true;
+    const int v = s ? atoi(s) : 2;
+    return v <= 1 ? 1 : std::min(v, FSP_MAX_GBUF);
 }
 
 // Choose the machine specialisation, warps per CTA and couple groups so that
@@ -1136,7 +1144,7 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                 if (tm_cols > 512) continue;
             }
             L.rt_bytes = nib ? 0 : 3 * (size_t)pl.maxm * 32 * npl * (pl.s16 ? 2 : 4);
-            L.off_rt = L.off_bar + 32;
+            L.off_rt = L.off_bar + 16 * FSP_MAX_GBUF; // mbarriers, counters, TMEM address
             L.list_bytes = pl.sparse ? align16(((size_t)pl.nrec + FSP_REC_SLACK + 4) * 8) : 0;
             L.off_list = align16(L.off_rt + (size_t)W * L.rt_bytes);
             L.off_tab = align16(L.off_list + (size_t)W * L.list_bytes);
@@ -1156,8 +1164,9 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                 }
                 // two or more groups: double-buffered (two group buffers) unless
                 // FSP_LB_DBUF=0 (one buffer, CTA barrier per group switch)
-                const bool db = Greal > 1 && dbuf_on();
-                if (L.off_tab + (db ? 2 : 1) * gb <= (size_t)optin) {
+                const int nb = Greal > 1 ? std::min(Greal, nbuf_want()) : 1;
+                const bool db = nb >= 2;
+                if (L.off_tab + nb * gb <= (size_t)optin) {
                     fsp_lb_plan c = pl;
                     L.group_bytes = gb;
                     c.L = L;
@@ -1165,8 +1174,8 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                     c.groups = Greal;
                     c.pairs_per_group = ppg;
                     c.warps = W;
-                    c.smem_bytes = L.off_tab + (db ? 2 : 1) * gb;
-                    c.dbuf = db;
+                    c.smem_bytes = L.off_tab + nb * gb;
+                    c.dbuf = db ? nb : 0;
                     c.tm_cols = tm_cols;
                     c.byte_rows = lay == 0;
                     // co-resident CTAs must fit the SM's 512 TMEM columns (an
@@ -1234,7 +1243,7 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.stride = stride;
     a.hi_mul = 0x10000u;
     a.tm_cols = (uint32_t)pl.tm_cols;
-    a.dbuf = pl.dbuf ? 1 : 0;
+    a.dbuf = pl.dbuf;
     a.woff = inst->max_p;
     // couple split for pools with fewer tiles than warp slots (latency-bound
     // otherwise: a 4,096-node pool is 32 tiles on 148 x 16 warps); the pool size
