@@ -146,7 +146,8 @@ __device__ __forceinline__ void tm_wait_ld(uint32_t (&a)[N], uint32_t (&b)[N])
     }
 }
 
-__device__ __forceinline__ int tm_half(uint32_t w, int hi) { return (int)((w >> (hi ? 16 : 0)) & 0xffffu); }
+// the low or high 16-bit half of a TMEM word, zero-extended: one PRMT
+__device__ __forceinline__ int tm_half(uint32_t w, int hi) { return (int)__byte_perm(w, 0u, hi ? 0x4432u : 0x4410u); }
 
 struct LbArgs {
     const uint8_t *tables; // groups x group_bytes
