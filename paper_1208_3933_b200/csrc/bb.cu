@@ -263,23 +263,21 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
                     }
                     crow4[q] = v;
                 }
-                // completion times: one max-plus scan over machines (lanes)
-                const int pk = lane < m ? ptm[j * m + lane] : 0;
-                const int ck = lane < m ? st.C[(size_t)src * m + lane] : 0;
-                int S = pk;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, S, o);
-                    if (lane >= o) S += y;
+            }
+            // completion times, lane t for child t: C'_0 = C_0 + p_j0,
+            // C'_k = max(C'_k-1, C_k) + p_jk, a serial max-plus pass over the
+            // machines per lane (all g children at once)
+            if (lane < g) {
+                const int32_t *pc = st.C + (size_t)src * m;
+                const int32_t *pj = ptm + (size_t)myj * m;
+                int32_t *cc = ch.C + (size_t)(c0 + lane) * m;
+                int prev = 0;
+#pragma unroll 4
+                for (int k = 0; k < m; ++k) {
+                    prev = max(prev, pc[k]) + pj[k];
+                    cc[k] = prev;
                 }
-                int M = ck - (S - pk);
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, M, o);
-                    if (lane >= o) M = max(M, y);
-                }
-                if (lane < m) ch.C[(size_t)(c0 + t) * m + lane] = S + M;
-                if (lane == 0) ch.dp[c0 + t] = d + 1;
+                ch.dp[c0 + lane] = d + 1;
             }
         }
         if (keep) {
