@@ -324,6 +324,12 @@ __global__ void __launch_bounds__(kPruneThreads)
                  unsigned long long *cand, int32_t *bcnt, unsigned long long *stats)
 {
     const int64_t C = *count;
+    // the grid covers the child buffer's capacity; blocks past this
+    // iteration's children only report an empty count
+    if ((int64_t)blockIdx.x * blockDim.x >= C) {
+        if (threadIdx.x == 0) bcnt[blockIdx.x] = 0;
+        return;
+    }
     const int inc = *inc_dev;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int survive = 0, pruned = 0, leaf = 0;
@@ -356,6 +362,7 @@ __global__ void __launch_bounds__(kPruneThreads)
     __shared__ int64_t s_dst[kPruneThreads];
     __shared__ int64_t s_src[kPruneThreads];
     const int64_t C = *count;
+    if ((int64_t)blockIdx.x * blockDim.x >= C) return; // past this iteration's children
     const int64_t top = first + (*off_B >> 32);
     const int inc = *inc_dev;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -374,14 +381,37 @@ __global__ void __launch_bounds__(kPruneThreads)
     __syncthreads();
     // warp-cooperative, coalesced row copies; rows are 16-byte aligned (stride
     // is a multiple of 8), so prefixes move as uint4s (eight job ids each)
+    // Four rows per warp in flight (loads of all four before their stores: the
+    // copy is latency-bound, one row per warp left most of HBM idle).
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
-    for (int k = wib; k < tot; k += nwb) {
-        const int64_t src = s_src[k], dst = s_dst[k];
-        const int d8 = (ch.dp[src] + 7) >> 3;
-        const uint4 *srow = reinterpret_cast<const uint4 *>(ch.pf + (size_t)src * stride);
-        uint4 *drow = reinterpret_cast<uint4 *>(st.pf + (size_t)dst * stride);
-        for (int q = lane; q < d8; q += 32) drow[q] = srow[q];
-        for (int q = lane; q < m; q += 32) st.C[(size_t)dst * m + q] = ch.C[(size_t)src * m + q];
+    constexpr int RU = 4;
+    for (int k0 = wib; k0 < tot; k0 += RU * nwb) {
+        int64_t src[RU], dst[RU];
+        int d8[RU];
+        uint4 v[RU];
+        int cv[RU];
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+            const int k = k0 + u * nwb;
+            d8[u] = 0;
+            if (k < tot) {
+                src[u] = s_src[k];
+                dst[u] = s_dst[k];
+                d8[u] = (ch.dp[src[u]] + 7) >> 3;
+                if (lane < d8[u]) v[u] = reinterpret_cast<const uint4 *>(ch.pf + (size_t)src[u] * stride)[lane];
+                if (lane < m) cv[u] = ch.C[(size_t)src[u] * m + lane];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+            if (k0 + u * nwb >= tot) continue;
+            uint4 *drow = reinterpret_cast<uint4 *>(st.pf + (size_t)dst[u] * stride);
+            const uint4 *srow = reinterpret_cast<const uint4 *>(ch.pf + (size_t)src[u] * stride);
+            if (lane < d8[u]) drow[lane] = v[u];
+            for (int q = lane + 32; q < d8[u]; q += 32) drow[q] = srow[q]; // rows beyond 256 jobs
+            if (lane < m) st.C[(size_t)dst[u] * m + lane] = cv[u];
+            for (int q = lane + 32; q < m; q += 32) st.C[(size_t)dst[u] * m + q] = ch.C[(size_t)src[u] * m + q];
+        }
     }
 }
 
