@@ -762,6 +762,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
 #pragma unroll
         for (int q = 0; q < NPL; ++q) lb[q] = 0;
         const bool ascending = resident == 0;
+        int kc = -1, rkv[NPL], akv[NPL]; // SPARSE TM: R_k - D and A_k of the last first machine
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) rkv[q] = akv[q] = 0;
         for (int gi = 0; gi < a.groups; ++gi) {
             const int g = dbuf ? gi : ascending ? gi : a.groups - 1 - gi;
             const long long sq = it * a.groups + gi;
@@ -792,8 +795,32 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 const int k = kv & 0xffff, l = kv >> 16;
                 // lines 06-07: timeOnM1 / timeOnM2 start at the RM minima, so
                 // e = t2 - t1 starts at R_l - R_k (>= 0)
-                int ee[NPL];
-                if constexpr (TM) {
+                int ee[NPL], fin[NPL]; // SPARSE TM: fin = A_k + Q_l (lines 18-19)
+                if constexpr (TM && SPARSE) {
+                    // short walks (B&B blocks): one TMEM round trip per couple,
+                    // R_k and A_k reloaded only when k changes ((k, l) order)
+                    uint32_t rl[NPLP], ql[NPLP];
+                    tm_ld<NPLP>(tbase + (0 * HM + (l >> 1)) * NPLP, rl);
+                    tm_ld<NPLP>(tbase + (2 * HM + (l >> 1)) * NPLP, ql);
+                    if (k != kc) {
+                        uint32_t rk[NPLP], ak[NPLP];
+                        tm_ld<NPLP>(tbase + (0 * HM + (k >> 1)) * NPLP, rk);
+                        tm_ld<NPLP>(tbase + (1 * HM + (k >> 1)) * NPLP, ak);
+                        tm_wait_ld<NPLP>(rk, ak);
+#pragma unroll
+                        for (int q = 0; q < NPL; ++q) {
+                            rkv[q] = tm_half(rk[q], k & 1) - woff;
+                            akv[q] = tm_half(ak[q], k & 1);
+                        }
+                        kc = k;
+                    }
+                    tm_wait_ld<NPLP>(rl, ql);
+#pragma unroll
+                    for (int q = 0; q < NPL; ++q) {
+                        ee[q] = tm_half(rl[q], l & 1) - rkv[q];
+                        fin[q] = akv[q] + tm_half(ql[q], l & 1);
+                    }
+                } else if constexpr (TM) {
                     uint32_t rl[NPLP], rk[NPLP];
                     tm_ld<NPLP>(tbase + (0 * HM + (l >> 1)) * NPLP, rl);
                     tm_ld<NPLP>(tbase + (0 * HM + (k >> 1)) * NPLP, rk);
@@ -900,7 +927,10 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                     for (int q = 0; q < NPL; ++q) ee[q] = (int)(ee[q] & 0xffff) - woff;
                 }
                 // lines 18-19: timeOnM2 = t1 + e with t1 = R_k + L_k at the end
-                if constexpr (TM) {
+                if constexpr (TM && SPARSE) {
+#pragma unroll
+                    for (int q = 0; q < NPL; ++q) lb[q] = max(lb[q], ee[q] + fin[q]);
+                } else if constexpr (TM) {
                     uint32_t ak[NPLP], ql[NPLP];
                     tm_ld<NPLP>(tbase + (1 * HM + (k >> 1)) * NPLP, ak);
                     tm_ld<NPLP>(tbase + (2 * HM + (l >> 1)) * NPLP, ql);
