@@ -189,7 +189,10 @@ def completion_times(p, pf, dp):
 
 
 @pytest.mark.parametrize("name,depth", [("ta021", 15), ("ta051", 40), ("ta091", 190),
-                                        ("ta091", 120), ("ta001", 10), ("ta111", 480)])
+                                        ("ta091", 120), ("ta001", 10), ("ta111", 480),
+                                        # live sets around 32 jobs per 128-node block: the
+                                        # inverse-position compaction and the scan both run
+                                        ("ta091", 168), ("ta091", 172), ("ta091", 176)])
 def test_parity_sibling_pools(torch, fsp, orc, name, depth):
     n, m, seed = inputs.TAILLARD_SEEDS[name]
     ptm = inputs.taillard(n, m, seed)
