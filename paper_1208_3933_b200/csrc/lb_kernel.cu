@@ -2,17 +2,18 @@
 //
 // Computes, for every node of a pool, the LB of Fig. 3 with the
 // readings R1-R6 of DESIGN.md §3.  Design:
-//   * one thread per sub-problem, as the paper maps it — here two
-//     sub-problems per thread, 64 per warp, so every table read of the couple
-//     walk is warp-uniform (a shared-memory broadcast) and feeds 64 nodes;
+//   * one thread per sub-problem, as the paper maps it — here four
+//     sub-problems per thread (two for generic m), 128 per warp, so every table
+//     read of the couple walk is warp-uniform (a shared-memory broadcast);
 //   * the per-couple tables (Johnson-with-lags order with each job's constants
 //     folded into an 8-byte record) are staged into shared memory by TMA bulk
-//     copies (cp.async.bulk + mbarrier), one couple group at a time when the
-//     whole set exceeds shared memory (200x20: 3 groups);
-//   * the unscheduled sets of a warp's 64 nodes are a transposed bitset
-//     U[job][warp] = {bits of nodes 0-31, bits of nodes 32-63}, built from
-//     coalesced reads of the prefix records; each record carries the absolute
-//     shared address of U[job][0], so one LOP3 (| 8*warp) addresses it;
+//     copies (cp.async.bulk + mbarrier), in couple groups held in two buffers
+//     when the whole set exceeds shared memory (200x20: 8 groups of 24);
+//   * the unscheduled sets of a warp's nodes are a transposed bitset, one row
+//     per job: a byte per lane (16-bit walk, m >= 10), 5-bit fields (long job
+//     lists) or one word per 32 nodes (m = 5, int32 walk); each record carries
+//     the row's offset, so one multiply-add addresses a lane's mask;
+//   * per-node heads/tails (R, A = R + L, Q) live in tensor memory (TMEM);
 //   * the walk of Fig. 3 lines 08-17 is carried in the difference form
 //     e = timeOnM2 - timeOnM1:
 //         e <- max(e + x_j, y_j)      (if j unscheduled)
