@@ -197,8 +197,7 @@ __global__ void plan_kernel(Nodes st, int64_t first, int64_t B, int n, int K, co
 // Branching (a7): one warp per parent; its unscheduled jobs of ascending rank
 // cur .. cur+g-1 become children prefix + j; lane t < g owns child
 // t.  Child completion times C'_0 = C_0 + p_j0, C'_k = max(C'_k-1, C_k) + p_jk
-// are one max-plus scan across lanes = machines:
-//   C'_k = S_k + max_{i<=k} (C_i - S_i-1),  S_k = sum_{i<=k} p_ji.
+// come from one serial pass over the machines per lane.
 // A parent with children left is copied to the kept buffer, cursor advanced.
 // Rows are 16-byte aligned (stride is a multiple of 8): copies move uint4s.
 __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t *__restrict__ off,
