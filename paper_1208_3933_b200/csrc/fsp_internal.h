@@ -37,7 +37,7 @@ struct fsp_lb_layout {
                                //   layout: one [(n+1)][urow_words] block per warp):
     int urow_words;            //   word warp*npl + q of job j's row = nodes q*32..q*32+31
     size_t off_ptm, ptm_bytes; // PTM int32 [n][mp4]
-    size_t off_bar;            // mbarriers, buffer release counters, TMEM address (16 B x FSP_MAX_GBUF)
+    size_t off_bar;            // mbarriers, buffer release counters, TMEM address (32 B x FSP_MAX_GBUF)
     size_t off_rt, rt_bytes;   // per warp: R, A (= R + L), Q, each [MAXM][32*npl]
     size_t off_list, list_bytes; // per warp (sparse walk): compacted records of a couple
     size_t off_tab;            // one couple group: [kl header][records]

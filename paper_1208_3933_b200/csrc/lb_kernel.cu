@@ -43,6 +43,11 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
 {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
@@ -330,10 +335,11 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
     constexpr int NPLP = NPL; // TMEM columns per (array, machine pair)
     constexpr int HM = (MAXM + 1) / 2, TCOLS = 3 * HM * NPLP;
     constexpr int HMP = (HM + 3) & ~3; // machine pairs per packed row, padded to 16 bytes
-    // barrier area (32 B): [0] mbarrier "group buffer 0 full" (with PTM), [1]
-    // "buffer 1 full", [2] release counters of the two buffers (u32 x 2), [3] TMEM
-    // base address
-    uint32_t *s_cnt = reinterpret_cast<uint32_t *>(s_bar + FSP_MAX_GBUF);
+    // barrier area (32 B per buffer): mbarriers "group buffer b full" (b = 0 also
+    // counts PTM), mbarriers "buffer b released by all warps", release counters,
+    // TMEM base address
+    uint64_t *s_emp = s_bar + FSP_MAX_GBUF;
+    uint32_t *s_cnt = reinterpret_cast<uint32_t *>(s_emp + FSP_MAX_GBUF);
     uint32_t *s_tm = s_cnt + FSP_MAX_GBUF;
     if constexpr (TM) {
         if (warp == 0) tm_alloc(s_tm, a.tm_cols);
@@ -372,6 +378,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
     if (threadIdx.x == 0) {
         for (int b = 0; b < FSP_MAX_GBUF; ++b) {
             mbar_init(s_bar + b, 1);
+            mbar_init(s_emp + b, W);
             s_cnt[b] = 0;
         }
         uint32_t gb = group_blob(0);
@@ -954,9 +961,13 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 __syncwarp();
                 if (lane == 0) {
                     const int b = (int)(sq % NB);
-                    __threadfence_block();
+                    // release this warp's reads of the buffer (mbarrier arrive); the
+                    // counter only elects the refilling warp, which then waits on the
+                    // "released" mbarrier (acquire) before the TMA overwrites it
+                    mbar_arrive(s_emp + b);
                     const uint32_t old = atomicAdd(&s_cnt[b], 1u);
                     if (old == (uint32_t)((sq / NB + 1) * W - 1) && sq + NB < nseq) {
+                        mbar_wait(s_emp + b, (uint32_t)((sq / NB) & 1));
                         const int gn = (int)((sq + NB) % a.groups);
                         const uint32_t gb = group_blob(gn);
                         fence_proxy_async();
@@ -1176,7 +1187,7 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                 if (tm_cols > 512) continue;
             }
             L.rt_bytes = nib ? 0 : 3 * (size_t)pl.maxm * 32 * npl * (pl.s16 ? 2 : 4);
-            L.off_rt = L.off_bar + 16 * FSP_MAX_GBUF; // mbarriers, counters, TMEM address
+            L.off_rt = L.off_bar + 32 * FSP_MAX_GBUF; // mbarriers, counters, TMEM address
             L.list_bytes = pl.sparse ? align16(((size_t)pl.nrec + FSP_REC_SLACK + 4) * 8) : 0;
             L.off_list = align16(L.off_rt + (size_t)W * L.rt_bytes);
             L.off_tab = align16(L.off_list + (size_t)W * L.list_bytes);
