@@ -10,7 +10,7 @@
  *   - a depth-first B&B with the four operators of §II-A and the
  *     forward branching of §II-B, ora_bb_dfs.
  *
- * Readings of passages the paper leaves silent or garbled are cited as R1..R18
+ * Readings of passages the paper leaves silent or garbled are cited as R1..R19
  * (taken from SURVEY.md §8(c) A1..A18).  No blocking, fusion or
  * reordering beyond what Fig. 3 states.  Nothing here is shared with the CUDA
  * path.
@@ -281,13 +281,43 @@ typedef struct {
     ora_bb_stats st;
 } dfs_ctx;
 
-typedef struct { int32_t lb, job; } kid;
+typedef struct { int32_t lb, idle, job; } kid;
 
+/* Best-first order among sons (R10): ascending LB; equal LBs by ascending
+ * idle time the son's job adds (R19), then by job id. */
 static int kid_cmp(const void *x, const void *y)
 {
     const kid *a = (const kid *)x, *b = (const kid *)y;
     if (a->lb != b->lb) return a->lb < b->lb ? -1 : 1;
+    if (a->idle != b->idle) return a->idle < b->idle ? -1 : 1;
     return a->job < b->job ? -1 : (a->job > b->job);
+}
+
+/* Completion times C[k] of the prefix on every machine (the
+ * recurrence of ora_makespan kept per machine). */
+static void prefix_completion(const ora_tables *t, const uint16_t *prefix, int32_t d, int32_t *C)
+{
+    for (int32_t k = 0; k < t->m; ++k) C[k] = 0;
+    for (int32_t i = 0; i < d; ++i) {
+        int32_t prev = 0;
+        for (int32_t k = 0; k < t->m; ++k) {
+            C[k] = imax(C[k], prev) + t->PTM[prefix[i] * t->m + k];
+            prev = C[k];
+        }
+    }
+}
+
+/* R19: idle time appending job j adds: machine k, free at C[k], waits until
+ * j leaves machine k-1; sum over k of (start of j on k) - C[k]. */
+static int32_t son_idle(const ora_tables *t, const int32_t *C, int32_t j)
+{
+    int32_t idle = 0, prev = 0;
+    for (int32_t k = 0; k < t->m; ++k) {
+        const int32_t start = imax(C[k], prev);
+        idle += start - C[k];
+        prev = start + t->PTM[j * t->m + k];
+    }
+    return idle;
 }
 
 /* Store a complete schedule (prefix[0..n)) if it improves on U. */
@@ -308,7 +338,8 @@ static void leaf(dfs_ctx *c)
 
 /* Decompose the node prefix[0..d) (branching: son i schedules job
  * J_i next), bound every son (Fig. 3), eliminate sons with LB >= U (R9),
- * and explore the rest depth-first in ascending (LB, job) order (R10). */
+ * and explore the rest depth-first in ascending (LB, idle, job) order (R10,
+ * R19). */
 static void dfs(dfs_ctx *c, int32_t d)
 {
     const ora_tables *t = c->t;
@@ -322,6 +353,8 @@ static void dfs(dfs_ctx *c, int32_t d)
         return;
     }
     kid *kids = (kid *)malloc(sizeof(kid) * (size_t)n);
+    int32_t *C = (int32_t *)malloc(sizeof(int32_t) * (size_t)t->m);
+    prefix_completion(t, c->prefix, d, C);
     int32_t nk = 0;
     for (int32_t j = 0; j < n; ++j) {
         if (c->scheduled[j]) continue;
@@ -339,6 +372,7 @@ static void dfs(dfs_ctx *c, int32_t d)
         c->st.bounded++;
         if (lb >= c->U) { c->st.pruned++; continue; }
         kids[nk].lb = lb;
+        kids[nk].idle = son_idle(t, C, j);
         kids[nk].job = j;
         ++nk;
     }
@@ -352,6 +386,7 @@ static void dfs(dfs_ctx *c, int32_t d)
         c->scheduled[kids[q].job] = 0;
     }
     free(kids);
+    free(C);
 }
 
 int ora_bb_dfs(const ora_tables *t, int32_t initial_ub, int64_t node_limit,
