@@ -4,7 +4,7 @@
  * Algorithm for the Flow-Shop Scheduling Problem", arXiv 1208.3933.
  *
  * Citations "P:a-b" are lines of the paper's LaTeX source.
- * Readings R1..R18 of silent or garbled passages are listed in DESIGN.md §3.
+ * Readings R1..R19 of silent or garbled passages are listed in DESIGN.md §3.
  *
  * Conventions for every entry point:
  *  - Return value: int status, FSP_OK (0) or a negative FSP_E* code; the
@@ -165,8 +165,11 @@ int fsp_bb_solve(const fsp_instance *inst, int32_t initial_ub, int64_t max_nodes
  * collectives).  A state holds one device-resident pool.
  *  fsp_bb_init        state for rank/world (rank r keeps the root's
  *                     descendants assigned to it).
- *  fsp_bb_step        up to `iters` expand/bound/prune iterations on stream;
- *                     synchronous (reads the pool size back).
+ *  fsp_bb_step        up to `iters` expand/bound/prune iterations.  The state
+ *                     owns a stream; the iterations are ordered after work
+ *                     already queued on cuda_stream, and later work on
+ *                     cuda_stream after them.  Synchronous (reads the pool
+ *                     size back).
  *  fsp_bb_ub_publish  writes (best << 32) | rank into a caller DEVICE int64
  *                     (stream-ordered), best = makespan of the schedule this
  *                     rank holds (INT32_MAX: none): the operand of a MIN
@@ -177,8 +180,18 @@ int fsp_bb_solve(const fsp_instance *inst, int32_t initial_ub, int64_t max_nodes
  *  fsp_bb_ub_get/set  the same exchange through a HOST int64 (gloo, tests).
  *  fsp_bb_pool_size   HOST out: open nodes in the pool.
  *  fsp_bb_export      move up to max_nodes open nodes into a DEVICE buffer of
- *                     fsp_bb_node_bytes(state) bytes per node (donor side).
+ *                     fsp_bb_node_bytes(state) bytes per node (donor side);
+ *                     the buffer is complete when the call returns.
  *  fsp_bb_import      append n nodes from such a DEVICE buffer (receiver).
+ *                     The copy runs on the state's stream, which is NOT
+ *                     ordered after the caller's streams: the buffer's
+ *                     contents must be complete before the call (e.g. after
+ *                     an NCCL recv, synchronise the stream it was queued on).
+ *  fsp_bb_debug_children  test hook: copy the last iteration's child pool
+ *                     (every child with its LB, pruned or not) to a HOST
+ *                     buffer [k][stride] u16 | [k] depth | [k][m] C | [k] LB,
+ *                     stride = n rounded up to 8; *n_out = k.  max_nodes = 0:
+ *                     *n_out = the number available, nothing copied.
  *  fsp_bb_result      incumbent and its permutation (HOST), FSP_ENOTFOUND if
  *                     this rank holds none.
  *  fsp_bb_get_stats   counters of this rank. */
@@ -193,6 +206,7 @@ int fsp_bb_pool_size(void *state, int64_t *n);
 int64_t fsp_bb_node_bytes(void *state);
 int fsp_bb_export(void *state, int64_t max_nodes, void *d_buf, int64_t *n_out);
 int fsp_bb_import(void *state, const void *d_buf, int64_t n);
+int fsp_bb_debug_children(void *state, int64_t max_nodes, void *h_buf, int64_t *n_out);
 int fsp_bb_result(void *state, int32_t *makespan_out, int32_t *perm_out);
 int fsp_bb_get_stats(void *state, fsp_bb_stats *stats);
 void fsp_bb_free(void *state);

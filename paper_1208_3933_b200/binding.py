@@ -26,7 +26,8 @@ EXPORTS = [
     "fsp_lb_eval_host", "fsp_lb_eval_sibling", "fsp_check", "fsp_lb_work", "fsp_bb_solve", "fsp_bb_init",
     "fsp_bb_step", "fsp_bb_ub_publish", "fsp_bb_ub_adopt", "fsp_bb_ub_get", "fsp_bb_ub_set",
     "fsp_bb_pool_size", "fsp_bb_node_bytes",
-    "fsp_bb_export", "fsp_bb_import", "fsp_bb_result", "fsp_bb_get_stats", "fsp_bb_free",
+    "fsp_bb_export", "fsp_bb_import", "fsp_bb_debug_children", "fsp_bb_result", "fsp_bb_get_stats",
+    "fsp_bb_free",
     "fsp_last_error", "fsp_version",
 ]
 
@@ -82,6 +83,7 @@ def lib():
             "fsp_bb_node_bytes": (i64, [vp]),
             "fsp_bb_export": (C.c_int, [vp, i64, vp, C.POINTER(i64)]),
             "fsp_bb_import": (C.c_int, [vp, vp, i64]),
+            "fsp_bb_debug_children": (C.c_int, [vp, i64, vp, C.POINTER(i64)]),
             "fsp_bb_result": (C.c_int, [vp, C.POINTER(i32), vp]),
             "fsp_bb_get_stats": (C.c_int, [vp, C.POINTER(BBStats)]),
             "fsp_bb_free": (None, [vp]),
@@ -229,8 +231,8 @@ class BBState:
         except Exception:
             pass
 
-    def step(self, iters: int = 1):
-        _check(lib().fsp_bb_step(self._h, int(iters), None))
+    def step(self, iters: int = 1, stream=None):
+        _check(lib().fsp_bb_step(self._h, int(iters), _stream(stream)))
 
     def pool_size(self) -> int:
         v = C.c_int64(0)
@@ -262,6 +264,23 @@ class BBState:
 
     def import_(self, d_buf_ptr: int, k: int):
         _check(lib().fsp_bb_import(self._h, C.c_void_p(d_buf_ptr), int(k)))
+
+    def debug_children(self, max_nodes: int = 1 << 30):
+        """The last iteration's child pool (test hook): (prefix u16 [k][stride],
+        depth [k], completion times [k][m], LB [k]) as numpy arrays."""
+        m, stride = self.inst.m, (self.n + 7) & ~7
+        k = C.c_int64(0)
+        _check(lib().fsp_bb_debug_children(self._h, 0, None, C.byref(k)))
+        cap = min(int(max_nodes), int(k.value))
+        buf = np.zeros(max(1, cap) * (stride * 2 + 8 + 4 * m), np.uint8)
+        _check(lib().fsp_bb_debug_children(self._h, cap, buf.ctypes.data, C.byref(k)))
+        k = int(k.value)
+        o = 0
+        pf = buf[o:o + k * stride * 2].view(np.uint16).reshape(k, stride); o += k * stride * 2
+        dp = buf[o:o + 4 * k].view(np.int32); o += 4 * k
+        Cc = buf[o:o + 4 * k * m].view(np.int32).reshape(k, m); o += 4 * k * m
+        lb = buf[o:o + 4 * k].view(np.int32)
+        return pf.copy(), dp.copy(), Cc.copy(), lb.copy()
 
     def result(self):
         ms = C.c_int32(0)

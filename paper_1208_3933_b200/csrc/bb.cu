@@ -5,15 +5,18 @@
 //   selection  (a9)  the top B open nodes of a device stack (deepest-first
 //                    batches replace the paper's host best-first list, R10);
 //   branching  (a7)  lazy: a popped parent generates its next K children
-//                    (prefix + j, j unscheduled, ascending j) and, if
-//                    it has more, goes back on the stack below them with an
-//                    advanced cursor (bounded memory); each
-//                    child's completion times come from its parent's in one step;
+//                    (prefix + j, j unscheduled), taken in ascending
+//                    order of the idle time j adds (R19), and, if it has more,
+//                    goes back on the stack below them with an advanced cursor
+//                    (bounded memory); each child's
+//                    completion times come from its parent's in one step;
 //   bounding   (a1-a5) the LB kernel on the child pool with the sparse-walk plan
 //                    (children of nearby parents share most of their
 //                    unscheduled set), pool size read on the device;
 //   elimination (a6) prune + scan + scatter: survivors (LB < incumbent) are
-//                    stream-compacted onto the stack in child order, parents
+//                    stream-compacted onto the stack, each parent's children
+//                    in descending (LB, idle, j) so its best child is on top
+//                    (best-first among siblings, R10/R19), parents
 //                    whose stored LB reached the incumbent are dropped at pop;
 //                    leaves (depth >= n-1: LB is the exact makespan, R6/P4) feed
 //                    a packed (makespan, index) atomicMin and commit_kernel
@@ -46,20 +49,25 @@ struct BBStatus {
 };
 
 // Open nodes, structure of arrays: prefix, depth, completion times C[m],
-// cursor (children already generated), LB from when the node was bounded.
+// cursor (children already generated), LB from when the node was bounded,
+// key (idle << 12 | j) of the last child generated.
 struct Nodes {
     uint16_t *pf = nullptr;
     int32_t *dp = nullptr, *C = nullptr, *cur = nullptr, *lb = nullptr;
+    long long *kl = nullptr; // key of the last child generated (-1: none yet)
 };
 
 struct BBState {
     const fsp_instance *inst;
     int rank, world, n, m, stride, K;
+    int64_t dive_iters;   // iterations of the first single-parent dive
     int64_t cap;          // stack capacity (nodes)
     int64_t base, size;   // open nodes live in [base, size)
     int64_t ccap;         // children per iteration (buffer capacity)
     int64_t kcap;         // parents per iteration
     Nodes st, kp, ch;     // stack, kept parents (scratch), children
+    unsigned long long *ch_key; // per child: (idle << 12) | j (R19 tie key)
+    int32_t *ord;         // child slot -> child record, siblings by descending (LB, key)
     long long *plan;      // per parent: (keep << 32) | children now
     int64_t *off;         // exclusive scan of plan; off[B] = (kept << 32) | children
     int64_t *d_count;     // children this iteration (LB pool size)
@@ -74,6 +82,8 @@ struct BBState {
     int32_t *d_perm;      // this rank's best permutation
     unsigned long long *d_stats; // [pruned, leaves]
     BBStatus *d_status, *h_status;
+    int64_t last_children; // children of the last iteration (still in ch)
+    cudaEvent_t ev_in, ev_out; // ordering against a caller's stream (fsp_bb_step)
     cudaStream_t stream;
     bool own_stream, sparse;
     fsp_bb_stats stats;
@@ -194,20 +204,22 @@ __global__ void plan_kernel(Nodes st, int64_t first, int64_t B, int n, int K, co
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(&stats[0], (unsigned long long)__popc(b));
 }
 
-// Branching (a7): one warp per parent; its unscheduled jobs of ascending rank
-// cur .. cur+g-1 become children prefix + j; lane t < g owns child
-// t.  Child completion times C'_0 = C_0 + p_j0, C'_k = max(C'_k-1, C_k) + p_jk
+// Branching (a7): one warp per parent; its unscheduled jobs of ascending
+// (idle, j) rank cur .. cur+g-1 (R19) become children prefix + j;
+// lane t < g owns child t.  Child completion times C'_0 = C_0 + p_j0, C'_k = max(C'_k-1, C_k) + p_jk
 // come from one serial pass over the machines per lane.
 // A parent with children left is copied to the kept buffer, cursor advanced.
 // Rows are 16-byte aligned (stride is a multiple of 8): copies move uint4s.
 __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t *__restrict__ off,
-                              Nodes ch, Nodes kp, const int32_t *__restrict__ ptm, int n, int m,
-                              int stride)
+                              Nodes ch, unsigned long long *ch_key, Nodes kp,
+                              const int32_t *__restrict__ ptm, int n, int m, int stride)
 {
-    extern __shared__ uint32_t bm_all[];
+    extern __shared__ unsigned long long ex_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int nw = (n + 31) >> 5;
-    uint32_t *bm = bm_all + wib * nw;
+    // per warp: keys[n] u64 | bm[nw] u32
+    unsigned long long *keys = ex_smem + (size_t)wib * (n + (nw + 1) / 2);
+    uint32_t *bm = reinterpret_cast<uint32_t *>(keys + n);
     const int s8 = stride >> 3; // uint4 per row
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; p < B; p += warps) {
@@ -219,6 +231,7 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
         const int keep = (int)((o1 >> 32) - (o0 >> 32));
         const int64_t c0 = o0 & 0xffffffffll;
         const int d8 = (d + 7) >> 3; // uint4 holding prefix entries
+        long long klast = -1;        // key of the last child generated now
         if (g > 0) {
             // scheduled-job bitmap from the prefix, eight ids per load
             for (int w = lane; w < nw; w += 32) bm[w] = 0;
@@ -233,19 +246,53 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
                 }
             }
             __syncwarp();
-            // lane t < g: the unscheduled job of rank cur + t
-            int myj = -1;
-            {
-                const int r = cur + lane;
-                int base = 0;
-                for (int w = 0; w < nw; ++w) {
-                    uint32_t freeb = ~bm[w];
-                    if (w == nw - 1 && (n & 31)) freeb &= (1u << (n & 31)) - 1;
-                    const int c = __popc(freeb);
-                    if (lane < g && myj < 0 && r < base + c) myj = w * 32 + (__fns(freeb, 0, r - base + 1));
-                    base += c;
+            // candidates: the unscheduled jobs, each keyed (idle << 12) | j by the
+            // idle time appending it opens on the machines (R19): machine k,
+            // free at C_k, waits until j leaves machine k-1.  Compacted in j
+            // order into keys[0..nc).
+            const int32_t cpar = lane < m ? st.C[(size_t)src * m + lane] : 0;
+            int nc = 0;
+            for (int w = 0; w < nw; ++w) {
+                const int j = w * 32 + lane;
+                const bool cand = j < n && !(bm[w] >> lane & 1);
+                const unsigned bal = __ballot_sync(0xffffffffu, cand);
+                if (!bal) continue;
+                long long idle = 0;
+                int prev = 0;
+                const int32_t *pj = ptm + (size_t)(cand ? j : 0) * m;
+                for (int k = 0; k < m; ++k) {
+                    const int ck = __shfl_sync(0xffffffffu, cpar, k);
+                    const int start = max(ck, prev);
+                    idle += start - ck;
+                    prev = start + pj[k];
                 }
+                if (cand)
+                    keys[nc + __popc(bal & ((1u << lane) - 1))] =
+                        ((unsigned long long)idle << 12) | (unsigned)j;
+                nc += __popc(bal);
             }
+            __syncwarp();
+            // children of this pop: the g smallest keys above the last key taken
+            // (= key ranks cur .. cur+g-1), one warp-min round per child
+            long long thr = st.kl[src];
+            unsigned long long mykey = 0ull;
+            for (int t = 0; t < g; ++t) {
+                unsigned long long best = ~0ull;
+                for (int i = lane; i < nc; i += 32) {
+                    const unsigned long long k = keys[i];
+                    if ((long long)k > thr && k < best) best = k;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+                    best = y < best ? y : best;
+                }
+                if (lane == t) mykey = best;
+                thr = (long long)best;
+            }
+            klast = thr;
+            const int myj = lane < g ? (int)(mykey & 0xfffu) : -1;
+            __syncwarp(); // keys are rewritten by the warp's next parent
             // prefixes: every child row = the parent's row with its job at d
             for (int t = 0; t < g; ++t) {
                 const int j = __shfl_sync(0xffffffffu, myj, t);
@@ -277,6 +324,7 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
                     cc[k] = prev;
                 }
                 ch.dp[c0 + lane] = d + 1;
+                ch_key[c0 + lane] = mykey;
             }
         }
         if (keep) {
@@ -287,6 +335,7 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
             if (lane == 0) {
                 kp.dp[dst] = d;
                 kp.cur[dst] = cur + g;
+                kp.kl[dst] = klast;
                 kp.lb[dst] = st.lb[src];
             }
         }
@@ -312,15 +361,41 @@ __global__ void restore_kernel(Nodes kp, const int64_t *off_B, int64_t first, No
         if (lane == 0) {
             st.dp[dst] = d;
             st.cur[dst] = kp.cur[q];
+            st.kl[dst] = kp.kl[q];
             st.lb[dst] = kp.lb[q];
         }
     }
 }
 
+// Best-first among siblings (R10, R19): one warp per parent; its g children
+// [c0, c0+g) get slots in descending (LB, key) order, so after compaction the
+// best child is the top of the stack and is popped first.
+__global__ void order_kernel(const int32_t *__restrict__ lb, const unsigned long long *__restrict__ key,
+                             int64_t B, const int64_t *__restrict__ off, int32_t *ord)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < B; p += warps) {
+        const int64_t c0 = off[p] & 0xffffffffll;
+        const int g = (int)((off[p + 1] & 0xffffffffll) - c0);
+        if (g == 0) continue;
+        const int mylb = lane < g ? lb[c0 + lane] : 0;
+        const unsigned long long myk = lane < g ? key[c0 + lane] : 0ull;
+        int r = 0;
+        for (int t = 0; t < g; ++t) {
+            const int l = __shfl_sync(0xffffffffu, mylb, t);
+            const unsigned long long k = __shfl_sync(0xffffffffu, myk, t);
+            r += (l > mylb) || (l == mylb && k > myk);
+        }
+        if (lane < g) ord[c0 + r] = (int32_t)(c0 + lane);
+    }
+}
+
 // Elimination (a6) + leaves (a8): count survivors per block.
 __global__ void __launch_bounds__(kPruneThreads)
-    prune_kernel(Nodes ch, const int64_t *count, int n, const int32_t *inc_dev,
-                 unsigned long long *cand, int32_t *bcnt, unsigned long long *stats)
+    prune_kernel(Nodes ch, const int32_t *__restrict__ ord, const int64_t *count, int n,
+                 const int32_t *inc_dev, unsigned long long *cand, int32_t *bcnt,
+                 unsigned long long *stats)
 {
     const int64_t C = *count;
     // the grid covers the child buffer's capacity; blocks past this
@@ -333,10 +408,11 @@ __global__ void __launch_bounds__(kPruneThreads)
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int survive = 0, pruned = 0, leaf = 0;
     if (i < C) {
-        const int d = ch.dp[i], lb = ch.lb[i];
+        const int32_t rec = ord[i];
+        const int d = ch.dp[rec], lb = ch.lb[rec];
         if (d >= n - 1) { // complete or forced completion: LB is its makespan (R6, P4)
             leaf = 1;
-            if (lb < inc) atomicMin(cand, ((unsigned long long)(unsigned)lb << 32) | (unsigned)i);
+            if (lb < inc) atomicMin(cand, ((unsigned long long)(unsigned)lb << 32) | (unsigned)rec);
         } else if (lb < inc) {
             survive = 1;
         } else {
@@ -355,8 +431,9 @@ __global__ void __launch_bounds__(kPruneThreads)
 
 // Stream compaction of the survivors onto the stack above the kept parents.
 __global__ void __launch_bounds__(kPruneThreads)
-    scatter_kernel(Nodes ch, const int64_t *count, const int64_t *off_B, int n, int m, int stride,
-                   const int32_t *inc_dev, const int64_t *__restrict__ boff, int64_t first, Nodes st)
+    scatter_kernel(Nodes ch, const int32_t *__restrict__ ord, const int64_t *count,
+                   const int64_t *off_B, int n, int m, int stride, const int32_t *inc_dev,
+                   const int64_t *__restrict__ boff, int64_t first, Nodes st)
 {
     __shared__ int64_t s_dst[kPruneThreads];
     __shared__ int64_t s_src[kPruneThreads];
@@ -366,16 +443,18 @@ __global__ void __launch_bounds__(kPruneThreads)
     const int inc = *inc_dev;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int survive = 0;
-    if (i < C) survive = ch.dp[i] < n - 1 && ch.lb[i] < inc;
+    const int32_t rec = i < C ? ord[i] : 0;
+    if (i < C) survive = ch.dp[rec] < n - 1 && ch.lb[rec] < inc;
     long long tot;
     const long long r = block_excl_scan(survive, tot);
     if (survive) {
         const int64_t dst = top + boff[blockIdx.x] + r;
         s_dst[r] = dst;
-        s_src[r] = i;
-        st.dp[dst] = ch.dp[i];
+        s_src[r] = rec;
+        st.dp[dst] = ch.dp[rec];
         st.cur[dst] = 0;
-        st.lb[dst] = ch.lb[i];
+        st.kl[dst] = -1;
+        st.lb[dst] = ch.lb[rec];
     }
     __syncthreads();
     // warp-cooperative, coalesced row copies; rows are 16-byte aligned (stride
@@ -475,6 +554,7 @@ void free_nodes(Nodes &x)
     cudaFree(x.C);
     cudaFree(x.cur);
     cudaFree(x.lb);
+    cudaFree(x.kl);
     x = Nodes();
 }
 
@@ -484,6 +564,8 @@ void bb_free(BBState *s)
     free_nodes(s->st);
     free_nodes(s->kp);
     free_nodes(s->ch);
+    cudaFree(s->ch_key);
+    cudaFree(s->ord);
     cudaFree(s->plan);
     cudaFree(s->off);
     cudaFree(s->d_count);
@@ -499,6 +581,8 @@ void bb_free(BBState *s)
     cudaFree(s->d_stats);
     cudaFree(s->d_status);
     if (s->h_status) cudaFreeHost(s->h_status);
+    if (s->ev_in) cudaEventDestroy(s->ev_in);
+    if (s->ev_out) cudaEventDestroy(s->ev_out);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
 }
@@ -509,7 +593,7 @@ int64_t env_i64(const char *name, int64_t dflt)
     return v ? atoll(v) : dflt;
 }
 
-size_t node_bytes(const BBState *s) { return (size_t)s->stride * 2 + 12 + (size_t)s->m * 4; }
+size_t node_bytes(const BBState *s) { return (size_t)s->stride * 2 + 20 + (size_t)s->m * 4; }
 
 cudaError_t alloc_nodes(Nodes &x, int64_t cnt, int stride, int m)
 {
@@ -518,6 +602,7 @@ cudaError_t alloc_nodes(Nodes &x, int64_t cnt, int stride, int m)
     if (e == cudaSuccess) e = cudaMalloc(&x.C, (size_t)cnt * m * 4);
     if (e == cudaSuccess) e = cudaMalloc(&x.cur, (size_t)cnt * 4);
     if (e == cudaSuccess) e = cudaMalloc(&x.lb, (size_t)cnt * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&x.kl, (size_t)cnt * 8);
     return e;
 }
 
@@ -537,15 +622,19 @@ cudaError_t copy_nodes(const BBState *s, Nodes dst, int64_t di, Nodes src, int64
         e = cudaMemcpyAsync(dst.cur + di, src.cur + si, (size_t)k * 4, cudaMemcpyDeviceToDevice, q);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(dst.lb + di, src.lb + si, (size_t)k * 4, cudaMemcpyDeviceToDevice, q);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dst.kl + di, src.kl + si, (size_t)k * 8, cudaMemcpyDeviceToDevice, q);
     return e;
 }
 
 // A flat buffer of k nodes viewed as node arrays:
-// [k][stride] u16 prefixes | [k] depth | [k][m] C | [k] cursor | [k] LB.
+// [k] last-key i64 | [k][stride] u16 prefixes | [k] depth | [k][m] C | [k] cursor | [k] LB.
 Nodes flat_view(const BBState *s, const void *buf, int64_t k)
 {
     uint8_t *b = static_cast<uint8_t *>(const_cast<void *>(buf));
     Nodes x;
+    x.kl = reinterpret_cast<long long *>(b);
+    b += (size_t)k * 8;
     x.pf = reinterpret_cast<uint16_t *>(b);
     b += (size_t)k * s->stride * 2;
     x.dp = reinterpret_cast<int32_t *>(b);
@@ -590,6 +679,9 @@ int push_host(BBState *s, const std::vector<uint16_t> &pf, const std::vector<int
         e = cudaMemcpyAsync(s->st.cur + at, zero.data(), 4 * k, cudaMemcpyHostToDevice, q);
     if (e == cudaSuccess) // never bounded: LB 0, never eliminated at pop
         e = cudaMemcpyAsync(s->st.lb + at, zero.data(), 4 * k, cudaMemcpyHostToDevice, q);
+    std::vector<long long> none((size_t)k, -1);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(s->st.kl + at, none.data(), 8 * k, cudaMemcpyHostToDevice, q);
     if (e == cudaSuccess) e = cudaStreamSynchronize(q);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "B&B push");
     s->size += k;
@@ -615,10 +707,16 @@ void device_scan(BBState *s, const long long *in64, const int32_t *in32, int64_t
 int bb_iterate(BBState *s)
 {
     const fsp_instance *inst = s->inst;
-    const int n = s->n, m = s->m, stride = s->stride, K = s->K;
+    const int n = s->n, m = s->m, stride = s->stride;
     cudaStream_t st = s->stream;
     const int64_t open = s->size - s->base;
     if (open <= 0) return FSP_OK;
+    // the first dive (a9): one parent per iteration, all its children (up to
+    // 32, best idle first) bounded and ordered, for the first dive_iters
+    // iterations: a depth-first descent along the best child that sets the
+    // first incumbent (SURVEY.md §8(d) C4 "first dive sets it"); then batches
+    const bool dive = s->stats.iterations < s->dive_iters;
+    const int K = dive ? 32 : s->K;
     // B parents: at most K children each fit the child buffer; the stack grows
     // by at most B*K per iteration and B*K*n over a descent, held under half
     // the capacity (the beam); n*K slots of headroom are always left
@@ -626,6 +724,7 @@ int bb_iterate(BBState *s)
     int64_t B = std::min<int64_t>(open, std::min<int64_t>(s->kcap, s->ccap / K));
     B = std::min<int64_t>(B, std::max<int64_t>(1, s->cap / 2 / ((int64_t)K * n)));
     B = std::min<int64_t>(B, std::max<int64_t>(1, (usable - s->size) / K));
+    if (dive) B = 1;
     if (s->size + B * K > s->cap) return fsp_fail(FSP_ENOMEM, "B&B stack full");
     const int64_t first = s->size - B;
 
@@ -633,10 +732,11 @@ int bb_iterate(BBState *s)
     plan_kernel<<<(unsigned)((B + pb - 1) / pb), pb, 0, st>>>(s->st, first, B, n, K, s->d_inc,
                                                               s->plan, s->d_stats);
     device_scan(s, s->plan, nullptr, B, s->off, s->d_count);
-    const int ewarps = 8;
-    const int eblocks = (int)std::min<int64_t>((B + ewarps - 1) / ewarps, 148 * 16);
-    expand_kernel<<<eblocks, ewarps * 32, ewarps * ((n + 31) / 32) * 4, st>>>(
-        s->st, first, B, s->off, s->ch, s->kp, inst->d_ptm32, n, m, stride);
+    const int ewarps = n > 1024 ? 1 : 4;
+    const int eblocks = (int)std::min<int64_t>((B + ewarps - 1) / ewarps, 148 * 32);
+    const size_t esmem = (size_t)ewarps * 8 * (n + ((n + 31) / 32 + 1) / 2);
+    expand_kernel<<<eblocks, ewarps * 32, esmem, st>>>(s->st, first, B, s->off, s->ch, s->ch_key,
+                                                       s->kp, inst->d_ptm32, n, m, stride);
     const int64_t *off_B = s->off + B; // (kept << 32) | children, on the device
     restore_kernel<<<eblocks, ewarps * 32, 0, st>>>(s->kp, off_B, first, s->st, m, stride);
     // bounding: pool size read on the device, C from the parents, sparse walk
@@ -644,12 +744,13 @@ int bb_iterate(BBState *s)
     int rc = fsp_launch_lb_dev(inst, s->ch.pf, stride, s->ch.dp, maxC, s->d_count, s->ch.C, m,
                                s->sparse, s->ch.lb, st);
     if (rc != FSP_OK) return rc;
+    order_kernel<<<eblocks, ewarps * 32, 0, st>>>(s->ch.lb, s->ch_key, B, s->off, s->ord);
     const int nblk = (int)((maxC + kPruneThreads - 1) / kPruneThreads);
-    prune_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->d_count, n, s->d_inc, s->d_cand, s->bcnt,
-                                                  s->d_stats);
+    prune_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->ord, s->d_count, n, s->d_inc, s->d_cand,
+                                                  s->bcnt, s->d_stats);
     device_scan(s, nullptr, s->bcnt, nblk, s->boff, nullptr);
-    scatter_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->d_count, off_B, n, m, stride, s->d_inc,
-                                                    s->boff, first, s->st);
+    scatter_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->ord, s->d_count, off_B, n, m, stride,
+                                                    s->d_inc, s->boff, first, s->st);
     commit_kernel<<<1, 256, 0, st>>>(s->ch, n, stride, s->d_inc, s->d_cand, s->d_perm, s->d_packed,
                                      s->rank, off_B, s->boff + nblk, s->d_status);
     cudaError_t e = cudaGetLastError();
@@ -658,6 +759,7 @@ int bb_iterate(BBState *s)
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "B&B iteration");
     s->size = first + s->h_status->kept + s->h_status->survivors;
+    s->last_children = s->h_status->children;
     s->stats.bounded += s->h_status->children;
     s->stats.branched += B;
     s->stats.iterations += 1;
@@ -683,7 +785,9 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     s->stride = (inst->n + 7) & ~7;
     s->initial_inc = initial_ub == INT32_MAX ? INT32_MAX : initial_ub + 1; // R9
     s->sparse = getenv("FSP_BB_SPARSE") ? atoi(getenv("FSP_BB_SPARSE")) != 0 : true;
-    s->K = (int)std::max<int64_t>(1, env_i64("FSP_BB_K", 8)); // children per parent per pop
+    // children per parent per pop: one lane per child in expand/order, K <= 32
+    s->K = (int)std::min<int64_t>(32, std::max<int64_t>(1, env_i64("FSP_BB_K", 8)));
+    s->dive_iters = std::max<int64_t>(0, env_i64("FSP_BB_DIVE", s->n));
     cudaError_t e = cudaSuccess;
     if (stream) {
         s->stream = static_cast<cudaStream_t>(stream);
@@ -695,14 +799,14 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     size_t freeb = 0, totalb = 0;
     if (e == cudaSuccess) e = cudaMemGetInfo(&freeb, &totalb);
     // children per iteration: enough to fill the GPU several times over
-    s->ccap = std::max<int64_t>(env_i64("FSP_BB_CHILDREN", 1 << 21), s->K);
+    s->ccap = std::max<int64_t>(env_i64("FSP_BB_CHILDREN", 1 << 21), 32);
     s->kcap = s->ccap;
     // the stack takes most of the free HBM (180 GB per B200)
     const double frac = getenv("FSP_BB_MEM_FRAC") ? atof(getenv("FSP_BB_MEM_FRAC")) : 0.5;
     const size_t buffers = (size_t)(s->ccap + s->kcap) * node_bytes(s);
     int64_t cap = freeb > buffers ? (int64_t)((double)(freeb - buffers) * frac / node_bytes(s)) : 0;
     cap = env_i64("FSP_BB_STACK", std::min<int64_t>(cap, (int64_t)1 << 31));
-    s->cap = std::max<int64_t>(cap, (int64_t)n * s->K * 4);
+    s->cap = std::max<int64_t>(cap, (int64_t)n * 32 * 4); // the dive pushes up to 32 per level
     const int64_t nblk = (s->ccap + kPruneThreads - 1) / kPruneThreads + 1;
     if (e == cudaSuccess) e = alloc_nodes(s->st, s->cap, s->stride, m);
     if (e == cudaSuccess) e = alloc_nodes(s->kp, s->kcap, s->stride, m);
@@ -710,6 +814,8 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     auto alloc = [&](void **p, size_t bytes) {
         if (e == cudaSuccess) e = cudaMalloc(p, bytes);
     };
+    alloc((void **)&s->ch_key, (size_t)s->ccap * 8);
+    alloc((void **)&s->ord, (size_t)s->ccap * 4);
     alloc((void **)&s->plan, (size_t)s->kcap * 8);
     alloc((void **)&s->off, (size_t)(s->kcap + 1) * 8);
     alloc((void **)&s->d_count, 8);
@@ -725,6 +831,8 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     alloc((void **)&s->d_stats, 16);
     alloc((void **)&s->d_status, sizeof(BBStatus));
     if (e == cudaSuccess) e = cudaMallocHost((void **)&s->h_status, sizeof(BBStatus));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMemcpy(s->d_inc, &s->initial_inc, 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(s->d_cand, 0xff, 8);
     if (e == cudaSuccess) e = cudaMemset(s->d_stats, 0, 16);
@@ -740,9 +848,13 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     // the depth-1 nodes j with j % world == r
     std::vector<uint16_t> pf;
     std::vector<int32_t> dp;
-    if (world == 1) {
-        pf.assign(s->stride, 0xffff);
-        dp.push_back(0);
+    if (world == 1 || n == 1) {
+        // (n == 1: the one depth-1 node is a complete schedule, which is only
+        // evaluated as a child; rank 0 starts from the root, the others empty)
+        if (rank == 0) {
+            pf.assign(s->stride, 0xffff);
+            dp.push_back(0);
+        }
     } else {
         for (int j = n - 1; j >= 0; --j) {
             if (j % world != rank) continue;
@@ -828,15 +940,52 @@ extern "C" int fsp_bb_init(const fsp_instance *inst, int32_t initial_ub, int32_t
     return rc;
 }
 
-extern "C" int fsp_bb_step(void *state, int32_t iters, void *)
+extern "C" int fsp_bb_step(void *state, int32_t iters, void *cuda_stream)
 {
     BBState *s = static_cast<BBState *>(state);
     if (!s || iters < 0) return fsp_fail(FSP_EINVAL, "bad B&B state");
-    for (int i = 0; i < iters && s->size > s->base; ++i) {
-        int rc = bb_iterate(s);
-        if (rc != FSP_OK) return rc;
+    // the iterations run on the state's stream, ordered after the work already
+    // queued on cuda_stream; later work on cuda_stream is ordered after them
+    cudaStream_t cs = static_cast<cudaStream_t>(cuda_stream);
+    cudaError_t e = cudaEventRecord(s->ev_in, cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s->stream, s->ev_in, 0);
+    if (e != cudaSuccess) return fsp_cuda_fail(e, "B&B step ordering");
+    int rc = FSP_OK;
+    for (int i = 0; i < iters && s->size > s->base && rc == FSP_OK; ++i) rc = bb_iterate(s);
+    if (rc == FSP_OK) rc = read_stats(s);
+    e = cudaEventRecord(s->ev_out, s->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, s->ev_out, 0);
+    if (e != cudaSuccess && rc == FSP_OK) rc = fsp_cuda_fail(e, "B&B step ordering");
+    return rc;
+}
+
+// Test hook: the child pool of the last iteration (every child bounded, pruned
+// or not), flat HOST layout [k][stride] u16 prefixes | [k] depth | [k][m] C |
+// [k] LB, k = min(max_nodes, children of that iteration).
+extern "C" int fsp_bb_debug_children(void *state, int64_t max_nodes, void *h_buf, int64_t *n_out)
+{
+    BBState *s = static_cast<BBState *>(state);
+    if (!s || !n_out || max_nodes < 0 || (max_nodes > 0 && !h_buf))
+        return fsp_fail(FSP_EINVAL, "bad debug arguments");
+    if (max_nodes == 0) { // query: children available
+        *n_out = s->last_children;
+        return FSP_OK;
     }
-    return read_stats(s);
+    const int64_t k = std::min(max_nodes, s->last_children);
+    *n_out = k;
+    if (k == 0) return FSP_OK;
+    uint8_t *b = static_cast<uint8_t *>(h_buf);
+    const size_t pfb = (size_t)k * s->stride * 2, cb = (size_t)k * s->m * 4;
+    cudaStream_t q = s->stream;
+    cudaError_t e = cudaMemcpyAsync(b, s->ch.pf, pfb, cudaMemcpyDeviceToHost, q);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(b + pfb, s->ch.dp, (size_t)k * 4, cudaMemcpyDeviceToHost, q);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(b + pfb + (size_t)k * 4, s->ch.C, cb, cudaMemcpyDeviceToHost, q);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(b + pfb + (size_t)k * 4 + cb, s->ch.lb, (size_t)k * 4,
+                            cudaMemcpyDeviceToHost, q);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(q);
+    return cuda_or(e, "debug children");
 }
 
 extern "C" int fsp_bb_ub_publish(void *state, int64_t *d_dst, void *stream)
@@ -895,7 +1044,7 @@ extern "C" int64_t fsp_bb_node_bytes(void *state)
 
 // Donor side: the shallowest open nodes (bottom of the stack, the largest
 // subtrees) go out as one flat buffer of fsp_bb_node_bytes per node:
-// [k][stride] u16 prefixes | [k] depth | [k][m] C | [k] cursor | [k] LB.
+// [k] last-key i64 | [k][stride] u16 prefixes | [k] depth | [k][m] C | [k] cursor | [k] LB.
 extern "C" int fsp_bb_export(void *state, int64_t max_nodes, void *d_buf, int64_t *n_out)
 {
     BBState *s = static_cast<BBState *>(state);

@@ -116,18 +116,21 @@ def distributed_bb(engine, dist, group=None, *, rank: int, world: int, device="c
     stop = False
     while True:
         engine.step(sync_every)
-        # incumbent: MIN all-reduce of (own best << 32 | rank)
-        g = _allreduce_min_i64(dist, group, engine.ub_get(), device)
-        engine.ub_set(g)
-        sizes = _allgather_i64(dist, group, engine.pool_size(), world, device)
+        # ONE collective per round: all-gather of [ub word, pool size, bounded,
+        # elapsed ms]; the MIN of the ub words is the global incumbent (low 32
+        # bits: its holder), the sums/max drive termination and the budget
+        st = engine.status_word(int((time.perf_counter() - t0) * 1e3), device)
+        out = torch.empty(world * 4, dtype=torch.int64, device=device)
+        dist.all_gather_into_tensor(out, st, group=group)
+        rows = out.view(world, 4).cpu().numpy()
+        engine.ub_set(int(rows[:, 0].min()))
+        sizes = [int(x) for x in rows[:, 1]]
         rounds += 1
         if sum(sizes) == 0:
             break
-        # budget: every rank sees the same summed counters -> same decision
-        bounded = _allgather_i64(dist, group, int(engine.stats()["bounded"]), world, device)
-        elapsed = _allreduce_min_i64(dist, group, -int((time.perf_counter() - t0) * 1e3), device)
-        if (time_limit_s > 0 and -elapsed >= time_limit_s * 1e3) or \
-                (bounded_budget > 0 and sum(bounded) >= bounded_budget):
+        # budget: every rank sees the same gathered counters -> same decision
+        if (time_limit_s > 0 and int(rows[:, 3].max()) >= time_limit_s * 1e3) or \
+                (bounded_budget > 0 and int(rows[:, 2].sum()) >= bounded_budget):
             stop = True
             break
         for donor, recv, k in plan_rebalance(sizes, max_chunk):
@@ -189,6 +192,19 @@ class DeviceEngine:
     def ub_set(self, word):
         self.state.ub_set(word)
 
+    def status_word(self, elapsed_ms, device):
+        """[ub word, pool size, bounded, elapsed ms] as an int64 tensor on the
+        collective's device; on CUDA the ub word is written device-to-device
+        by fsp_bb_ub_publish (stream-ordered before the collective)."""
+        import torch
+        t = torch.tensor([0, self.pool_size(), int(self.stats()["bounded"]), elapsed_ms],
+                         dtype=torch.int64, device=device)
+        if t.is_cuda:
+            self.state.ub_publish(t[0:1])
+        else:
+            t[0] = self.ub_get()
+        return t
+
     def stats(self):
         return self.state.stats()
 
@@ -207,6 +223,10 @@ class DeviceEngine:
         return (out if self.comm == self.device else out.to(self.comm)), got
 
     def import_nodes(self, buf, k):
+        import torch
         if buf.device.type != "cuda":
             buf = buf.to(self.device)
+        # an NCCL recv only orders torch's current stream; fsp_bb_import copies
+        # on the state's own stream, so the data must have landed first
+        torch.cuda.current_stream(buf.device).synchronize()
         self.state.import_(buf.data_ptr(), k)

@@ -101,6 +101,11 @@ class HostEngine:
     def ub_set(self, word):
         self.inc = min(self.inc, fdist.unpack_ub(word)[0])
 
+    def status_word(self, elapsed_ms, device):
+        import torch
+        return torch.tensor([self.ub_get(), self.pool_size(), self.bounded, elapsed_ms],
+                            dtype=torch.int64, device=device)
+
     def stats(self):
         return {"bounded": self.bounded}
 

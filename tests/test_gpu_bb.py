@@ -75,10 +75,69 @@ def test_bb_m2_johnson(fsp, orc):
         assert rc == 0 and ms == orc.makespan(p, order) == orc.makespan(p, perm)
 
 
-def test_bb_ta002(fsp, orc):
-    p = inputs.instance("ta002")
-    rc, ms, perm, st = fsp.Instance(p).bb_solve()
-    assert rc == 0 and ms == 1359 and orc.makespan(p, perm) == 1359
+@pytest.mark.parametrize("name,opt", [("ta001", 1278), ("ta002", 1359), ("ta003", 1081),
+                                      ("ta004", 1293)])
+def test_bb_taillard_optimum(fsp, orc, name, opt):
+    # BASELINE.json configs[0]: full B&B from the root (no initial UB) to the
+    # optimum; ta002-ta004 optima recalled (tests/golden/taillard_optima.txt)
+    p = inputs.instance(name)
+    rc, ms, perm, st = fsp.Instance(p).bb_solve(2**31 - 1, 0, 120.0)
+    assert rc == 0 and ms == opt and orc.makespan(p, perm) == opt
+    assert sorted(perm.tolist()) == list(range(p.shape[0]))
+    # and the proof: nothing at or below opt - 1
+    rc, _, _, _ = fsp.Instance(p).bb_solve(opt - 1, 0, 120.0)
+    assert rc == fsp.FSP_ENOTFOUND
+
+
+def _completion(p, row, d):
+    m = p.shape[1]
+    C = np.zeros(m, np.int64)
+    for j in row[:d]:
+        prev = 0
+        for k in range(m):
+            C[k] = max(C[k], prev) + int(p[j, k])
+            prev = C[k]
+    return C
+
+
+@pytest.mark.parametrize("name,snapshots,sample", [("ta001", (1, 2, 5, 20, 60), 0),
+                                                   ("ta021", (1, 3, 10, 40), 4000),
+                                                   ("ta091", (1, 4, 30, 200), 1500)])
+def test_bb_child_pool_lbs_match_oracle(fsp, orc, name, snapshots, sample):
+    """Element-wise parity of the device B&B's bounding step: after a number of
+    iterations, the last iteration's child pool (prefixes built by expand,
+    completion times carried from the parents, LBs from the sparse-walk plan
+    with the pool size read on the device) is exported and every child's LB
+    (sample = 0) or a random sample of them is recomputed by the oracle."""
+    p = inputs.instance(name)
+    n = p.shape[0]
+    inst = fsp.Instance(p)
+    T = orc.Tables(p)
+    bb = fsp.BBState(inst)
+    rng = np.random.default_rng(7)
+    done = 0
+    checked = 0
+    for it in snapshots:
+        bb.step(it - done)
+        done = it
+        if bb.pool_size() == 0:
+            break
+        pf, dp, Cc, lb = bb.debug_children()
+        k = len(dp)
+        if k == 0:      # every popped parent was eliminated at pop (R9)
+            continue
+        idx = np.arange(k) if sample == 0 or k <= sample else np.sort(
+            np.concatenate([rng.choice(k - 32, sample - 32, replace=False), np.arange(k - 32, k)]))
+        want = T.lb_eval(pf[idx], dp[idx])
+        bad = np.nonzero(want != lb[idx])[0]
+        assert bad.size == 0, (name, it, idx[bad[:5]], lb[idx][bad[:5]], want[bad[:5]])
+        for i in idx[:: max(1, len(idx) // 200)]:
+            d = int(dp[i])
+            row = pf[i, :d].astype(np.int64)
+            assert len(set(row.tolist())) == d and row.max(initial=0) < n
+            assert (Cc[i] == _completion(p, row, d)).all()
+        checked += len(idx)
+    assert checked > 0
 
 
 def test_bb_budget(fsp, orc):
@@ -152,3 +211,71 @@ def test_distributed_driver_nccl_world1(fsp, orc):
         assert orc.makespan(p, res.perm) == opt
     finally:
         dist.destroy_process_group()
+
+
+def _gloo_device_worker(rank, world, port, ptm, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["FSP_BB_MEM_FRAC"] = "0.05"
+    os.environ["FSP_BB_CHILDREN"] = str(1 << 16)
+    from paper_1208_3933_b200 import binding
+    from paper_1208_3933_b200 import dist as fdist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        inst = binding.Instance(ptm)
+        state = binding.BBState(inst, 2**31 - 1, rank, world)
+        eng = fdist.DeviceEngine(state, "cuda", "cpu")
+        # forced imbalance: rank 1 hands its whole start pool to rank 0, so
+        # the work stealing has to move nodes back
+        nb = eng.node_bytes
+        if rank == 1:
+            buf, got = eng.export_nodes(state.pool_size())
+            dist.send(torch.tensor([got]), 0)
+            dist.send(buf.cpu(), 0)
+        else:
+            hdr = torch.zeros(1, dtype=torch.int64)
+            dist.recv(hdr, 1)
+            k = int(hdr.item())
+            buf = torch.empty(k * nb, dtype=torch.uint8)
+            dist.recv(buf, 1)
+            eng.import_nodes(buf, k)
+        sizes0 = state.pool_size()
+        res = fdist.distributed_bb(eng, dist, rank=rank, world=world, device="cpu", sync_every=1,
+                                   max_chunk=256)
+        q.put((rank, sizes0, res.status, res.makespan, res.perm.tolist(), res.moved))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_bb_world2_one_gpu_stealing(fsp, orc):
+    """dist.distributed_bb at world 2 (two processes sharing cuda:0, gloo
+    collectives, device engines): rank 1 starts empty, nodes must move
+    (moved > 0), and both ranks report the oracle optimum."""
+    import socket
+
+    import torch.multiprocessing as mp
+    rng = np.random.default_rng(21)
+    p = rng.integers(1, 99, (13, 6)).astype(np.int32)
+    opt = orc.Tables(p).bb_dfs()[1]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_device_worker, args=(r, 2, port, p, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = sorted(q.get(timeout=300) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert out[1][1] == 0                       # rank 1 started empty
+    assert all(o[2] == 0 and o[3] == opt for o in out), (out, opt)
+    assert out[0][4] == out[1][4] and orc.makespan(p, out[0][4]) == opt
+    assert out[0][5] > 0                        # work stealing moved nodes
