@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="ta091")
     ap.add_argument("--pool", type=int, default=1 << 20)
+    ap.add_argument("--strong-total", type=int, default=0,
+                    help="strong scaling: ranks bound contiguous shards of ONE pool of this "
+                         "many nodes (SURVEY.md §8(d) C4: 4M total) instead of 1M each")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-bb", action="store_true")
     ap.add_argument("--bb-seconds", type=float, default=10.0)
@@ -76,16 +79,28 @@ def algorithmic_ops(n, m, depth):
     return int((2 * d * m + npr * (3 * m - 2) + npr * m + P * n + 4 * P * npr + 2 * P).sum())
 
 
+# ALU-pipe throughput measured on this pool's B200 by tools/ubench/ipipe.cu
+# (profiles/r02/ipipe_b200.txt): VIMNMX / VIMNMX.U16x2 0.496 warp-instructions
+# per clock per SMSP (VIADDMNMX.U16x2 0.462 with the loop's own IADD in the
+# same pipe), i.e. the ALU pipe is half rate: 64 lane-ops/clk/SM.
+ALU_PIPE_WARP_INSTR_PER_CLK_SMSP = 0.496
+
+
 def alu_peak_tops():
-    """Integer issue peak: 148 SMs x 4 SMSPs x 32 lanes x 1 warp-instr/clk at
-    the max SM clock (clock from MEASURED_PEAKS.json)."""
+    """Roofline denominator: the measured ALU-pipe rate x 2
+    algorithmic ops per fused max-plus instruction (VIADDMNMX: add + max) x 32
+    lanes x 4 SMSPs x 148 SMs at the max SM clock (MEASURED_PEAKS.json).
+    Also returns the issue ceiling (1 warp-instruction/clk/SMSP) in lane-instr/s
+    and the ALU-pipe ceiling in lane-instr/s."""
     mhz = 1965.0
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             mhz = float(json.load(f).get("sm_max_mhz", mhz))
     except Exception:
         pass
-    return 148 * 4 * 32 * mhz * 1e6 / 1e12, mhz
+    lanes = 148 * 4 * 32 * mhz * 1e6
+    alu = lanes * ALU_PIPE_WARP_INSTR_PER_CLK_SMSP
+    return 2 * alu / 1e12, mhz, lanes / 1e12, alu / 1e12
 
 
 class ClockSampler:
@@ -376,7 +391,14 @@ def main():
     cfg = a.config
     n, m, seed = inputs.TAILLARD_SEEDS[cfg]
     ptm = inputs.taillard(n, m, seed)
-    pf, dp = inputs.pool_d1(n, a.pool, inputs.pool_seed(cfg) + 1000 * rank)
+    if a.strong_total > 0:
+        # strong scaling: rank r bounds nodes [lo, hi) of one seeded pool
+        from paper_1208_3933_b200 import dist as fdist
+        lo, hi = fdist.shard(a.strong_total, rank, world)
+        a.pool = hi - lo
+        pf, dp = inputs.pool_d1(n, a.pool, inputs.pool_seed(cfg), first=lo)
+    else:
+        pf, dp = inputs.pool_d1(n, a.pool, inputs.pool_seed(cfg) + 1000 * rank)
     stride = pf.shape[1]
     inst = binding.Instance(ptm)
     d_pf = torch.from_numpy(pf.view(np.int16)).cuda()
@@ -410,11 +432,12 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = a.pool * world * a.steps / (ms_max / 1e3)
+    total_nodes = a.strong_total if a.strong_total > 0 else a.pool * world
+    value = total_nodes * a.steps / (ms_max / 1e3)
 
     # roofline: algorithmic integer ops per launch / mean launch time
     ops = algorithmic_ops(n, m, dp)
-    peak, mhz = alu_peak_tops()
+    peak, mhz, issue_peak, alu_pipe_peak = alu_peak_tops()
     achieved = ops / (ms / a.steps / 1e3) / 1e12
     traffic, _ = ncu_traffic(cfg)
 
@@ -437,7 +460,7 @@ def main():
         dt = float(tt.item())
         if not torch.equal(h_lb, d_lb.cpu()):
             raise SystemExit("host-API LBs differ from device LBs")
-        e2e = {"value": a.pool * world * a.steps / dt, "unit": UNIT,
+        e2e = {"value": total_nodes * a.steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": int(pf.nbytes + dp.nbytes),
                "d2h_bytes_per_step": int(a.pool * 4)}
 
@@ -489,18 +512,28 @@ def main():
 
     if rank == 0:
         cfgd = workload(cfg, a.pool, world)
+        if a.strong_total > 0:
+            cfgd["total_pool"] = a.strong_total
+            cfgd["workload"] = cfgd["workload"].replace(f"D1 pool {a.pool} nodes/GPU",
+                                                        f"D1 pool {a.strong_total} nodes sharded")
+        cfgd["launch"] = inst.launch_info(a.pool)
         info = inst.info
         cfgd["lb_kernel"] = {k: info[k] for k in ("groups", "pairs_per_group", "warps_per_cta",
                                                   "ctas_per_sm", "smem_bytes", "maxm")}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": max(a.warmup, 3), "ms_per_step": ms_max / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "scaling": "strong" if a.strong_total > 0 else "weak", "vs_baseline": None,
+            "dtype": "u16 (walk) / int32 (bounds)", "data": "synthetic",
             "config": cfgd,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Top/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "peak_note": f"int issue peak 148 SM x 128 lanes x {mhz:.0f} MHz "
-                                      "(DESIGN.md §7)",
+                         "peak_note": "measured ALU pipe (profiles/r02/ipipe_b200.txt: "
+                                      f"{ALU_PIPE_WARP_INSTR_PER_CLK_SMSP} warp-instr/clk/SMSP) x 2 "
+                                      "ops per fused VIADDMNMX x 148 SM x 4 SMSP x 32 lanes x "
+                                      f"{mhz:.0f} MHz (DESIGN.md §7)",
+                         "alu_pipe_peak_tlane_instr_s": alu_pipe_peak,
+                         "issue_peak_tlane_instr_s": issue_peak,
                          "ops_per_launch": ops},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": a.steps,
             "clocks": clk.summary(), "bb": bb,

@@ -77,6 +77,28 @@ typedef struct {
 
 int fsp_instance_get_info(const fsp_instance *inst, fsp_instance_info *info);
 
+/* fsp_lb_launch_info — the launch shape fsp_lb_eval (sibling = 0) or
+ * fsp_lb_eval_sibling / the B&B bounding step (sibling = 1) uses for a pool
+ * of `pool` nodes (tests and bench.py report it; no device work). */
+typedef struct {
+    int32_t grid;             /* persistent CTAs                              */
+    int32_t warps_per_cta;
+    int32_t split;            /* warps sharing one 32*npl-node tile (couple split) */
+    int32_t iterations;       /* tile iterations per CTA                      */
+    int32_t groups;           /* couple groups cycled through shared memory   */
+    int32_t pairs_per_group;
+    int32_t group_buffers;    /* 1: one buffer + CTA barrier; >= 2: TMA ring  */
+    int32_t nodes_per_lane;
+    int32_t row_layout;       /* unscheduled-set rows: 0 word per 32 nodes,
+                                 1 byte per lane, 2 5-bit fields per lane     */
+    int32_t tmem_cols;        /* TMEM columns per CTA (0: heads in smem)      */
+    int32_t sparse_walk;      /* 1: walk over the block's live jobs only      */
+    int32_t smem_bytes;
+} fsp_lb_launch;
+
+int fsp_lb_launch_info(const fsp_instance *inst, int64_t pool, int32_t sibling,
+                       fsp_lb_launch *out);
+
 /* ------------------------------------------------------------------- bounding
  * fsp_lb_eval — the bounding operator of §III-A applied to a pool of
  * sub-problems: lb_out[i] = LB of node i, the lower bound of

@@ -22,7 +22,8 @@ _NAMES = {0: "FSP_OK", -1: "FSP_EINVAL", -2: "FSP_ERANGE", -3: "FSP_ENOMEM", -4:
 
 # every symbol include/fsp.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "fsp_instance_load", "fsp_instance_free", "fsp_instance_get_info", "fsp_lb_eval",
+    "fsp_instance_load", "fsp_instance_free", "fsp_instance_get_info", "fsp_lb_launch_info",
+    "fsp_lb_eval",
     "fsp_lb_eval_host", "fsp_lb_eval_sibling", "fsp_check", "fsp_lb_work", "fsp_bb_solve", "fsp_bb_init",
     "fsp_bb_step", "fsp_bb_ub_publish", "fsp_bb_ub_adopt", "fsp_bb_ub_get", "fsp_bb_ub_set",
     "fsp_bb_pool_size", "fsp_bb_node_bytes",
@@ -46,6 +47,13 @@ class InstanceInfo(C.Structure):
                 ("nodes_per_lane", C.c_int32), ("walk16", C.c_int32)]
 
 
+class LaunchInfo(C.Structure):
+    _fields_ = [(f, C.c_int32) for f in (
+        "grid", "warps_per_cta", "split", "iterations", "groups", "pairs_per_group",
+        "group_buffers", "nodes_per_lane", "row_layout", "tmem_cols", "sparse_walk",
+        "smem_bytes")]
+
+
 class BBStats(C.Structure):
     _fields_ = [("bounded", C.c_int64), ("branched", C.c_int64), ("pruned", C.c_int64),
                 ("leaves", C.c_int64), ("iterations", C.c_int64), ("wall_s", C.c_double)]
@@ -66,6 +74,7 @@ def lib():
             "fsp_instance_load": (C.c_int, [vp, i32, i32, C.POINTER(vp)]),
             "fsp_instance_free": (None, [vp]),
             "fsp_instance_get_info": (C.c_int, [vp, C.POINTER(InstanceInfo)]),
+            "fsp_lb_launch_info": (C.c_int, [vp, i64, i32, C.POINTER(LaunchInfo)]),
             "fsp_lb_eval": (C.c_int, [vp, vp, i32, vp, i64, vp, vp]),
             "fsp_lb_eval_host": (C.c_int, [vp, vp, i32, vp, i64, vp]),
             "fsp_lb_eval_sibling": (C.c_int, [vp, vp, i32, vp, vp, i64, vp, vp]),
@@ -151,6 +160,12 @@ class Instance:
         inf = InstanceInfo()
         _check(lib().fsp_instance_get_info(self._h, C.byref(inf)))
         return {f: getattr(inf, f) for f, _ in InstanceInfo._fields_}
+
+    def launch_info(self, pool: int, sibling: bool = False) -> dict:
+        """fsp_lb_launch_info: the bounding kernel's launch shape for a pool."""
+        li = LaunchInfo()
+        _check(lib().fsp_lb_launch_info(self._h, int(pool), int(bool(sibling)), C.byref(li)))
+        return {f: getattr(li, f) for f, _ in LaunchInfo._fields_}
 
     def lb_eval(self, prefix, depth, out=None, stream=None):
         """fsp_lb_eval on torch CUDA tensors: prefix uint16-compatible

@@ -210,3 +210,28 @@ extern "C" int fsp_instance_get_info(const fsp_instance *inst, fsp_instance_info
     info->walk16 = pl.s16 ? 1 : 0;
     return FSP_OK;
 }
+
+extern "C" int fsp_lb_launch_info(const fsp_instance *inst, int64_t pool, int32_t sibling,
+                                  fsp_lb_launch *out)
+{
+    if (!inst || !out || pool < 0) return fsp_fail(FSP_EINVAL, "bad launch-info arguments");
+    const fsp_lb_plan &pl = sibling ? inst->plan_bb : inst->plan;
+    const int tn = 32 * pl.npl;
+    const int split = fsp_lb_split(pl, pool);
+    const int64_t tiles = (pool + tn - 1) / tn;
+    const int64_t per_iter = (int64_t)(pl.warps / split) * pl.grid;
+    out->grid = pl.grid;
+    out->warps_per_cta = pl.warps;
+    out->split = split;
+    out->iterations = (int32_t)((tiles + per_iter - 1) / per_iter);
+    out->groups = pl.groups;
+    out->pairs_per_group = pl.pairs_per_group;
+    out->group_buffers = pl.dbuf >= 2 ? pl.dbuf : 1;
+    out->nodes_per_lane = pl.npl;
+    // 0: one word per 32 nodes (lane-major), 1: a byte per lane, 2: 5-bit fields
+    out->row_layout = !(pl.s16 && pl.maxm >= 10) ? 0 : pl.byte_rows ? 1 : 2;
+    out->tmem_cols = pl.tm_cols;
+    out->sparse_walk = pl.sparse ? 1 : 0;
+    out->smem_bytes = (int32_t)pl.smem_bytes;
+    return FSP_OK;
+}

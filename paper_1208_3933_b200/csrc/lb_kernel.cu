@@ -1247,6 +1247,23 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     return fsp_fail(FSP_ERANGE, "instance tables do not fit in shared memory");
 }
 
+// Couple split for pools with fewer tiles than warp slots (latency-bound
+// otherwise: a 4,096-node pool is 32 tiles on 148 x 16 warps); the pool size
+// of a device-sized launch (B&B) is only bounded by `pool`.
+int fsp_lb_split(const fsp_lb_plan &pl, int64_t pool)
+{
+    int split = 1;
+    const int64_t tiles = (pool + 32 * pl.npl - 1) / (32 * pl.npl);
+    const int64_t slots = (int64_t)pl.grid * pl.warps;
+    while (split < pl.warps && tiles * split * 2 <= slots) split *= 2;
+    if (const char *e = getenv("FSP_LB_SPLIT")) { // experiments and tests: a power of two
+        const int v = std::max(1, std::min(pl.warps, atoi(e)));
+        for (split = 1; split * 2 <= v;) split *= 2;
+    }
+    while (pl.warps % split) split /= 2;
+    return split;
+}
+
 int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                   const int32_t *depth, int64_t pool, int32_t *lb_out, cudaStream_t s)
 {
@@ -1288,20 +1305,7 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.tm_cols = (uint32_t)pl.tm_cols;
     a.dbuf = pl.dbuf;
     a.woff = inst->max_p;
-    // couple split for pools with fewer tiles than warp slots (latency-bound
-    // otherwise: a 4,096-node pool is 32 tiles on 148 x 16 warps); the pool size
-    // of a device-sized launch (B&B) is only bounded by `pool`
-    a.split = 1;
-    {
-        const int64_t tiles = (pool + 32 * pl.npl - 1) / (32 * pl.npl);
-        const int64_t slots = (int64_t)pl.grid * pl.warps;
-        while (a.split < pl.warps && tiles * a.split * 2 <= slots) a.split *= 2;
-        if (const char *e = getenv("FSP_LB_SPLIT")) { // experiments: a power of two
-            const int v = std::max(1, std::min(pl.warps, atoi(e)));
-            for (a.split = 1; a.split * 2 <= v;) a.split *= 2;
-        }
-        while (pl.warps % a.split) a.split /= 2;
-    }
+    a.split = fsp_lb_split(pl, pool);
     if (a.split > 1 && pool > 0) { // R1: every LB is a max starting at 0
         cudaError_t e = cudaMemsetAsync(lb_out, 0, sizeof(int32_t) * (size_t)pool, s);
         if (e != cudaSuccess) return fsp_cuda_fail(e, "lb_out clear");

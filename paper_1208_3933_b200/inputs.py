@@ -82,15 +82,19 @@ def default_stride(n: int) -> int:
     return (n + 7) // 8 * 8
 
 
-def random_prefixes(n: int, depth: np.ndarray, seed: int, stride: int | None = None):
-    """Uniformly random d-prefixes (partial Fisher-Yates, counter-based)."""
+def random_prefixes(n: int, depth: np.ndarray, seed: int, stride: int | None = None,
+                    first: int = 0):
+    """Uniformly random d-prefixes (partial Fisher-Yates, counter-based; node i
+    of the pool draws with counter first + i, so any slice of a pool can be
+    generated on its own)."""
     N = depth.shape[0]
     stride = default_stride(n) if stride is None else stride
     perm = np.tile(np.arange(n, dtype=np.uint16), (N, 1))
     rows = np.arange(N)
+    ctr = rows + first
     dmax = int(depth.max()) if N else 0
     for i in range(min(dmax, n - 1)):
-        r = _draw(seed, 1 + i, rows)
+        r = _draw(seed, 1 + i, ctr)
         j = (i + (r % np.uint64(n - i))).astype(np.int64)
         a = perm[:, i].copy()
         perm[:, i] = perm[rows, j]
@@ -102,11 +106,12 @@ def random_prefixes(n: int, depth: np.ndarray, seed: int, stride: int | None = N
     return out
 
 
-def pool_d1(n: int, N: int, seed: int, stride: int | None = None):
-    """Recipe D1: returns (prefix uint16[N][stride], depth int32[N])."""
-    rows = np.arange(N)
+def pool_d1(n: int, N: int, seed: int, stride: int | None = None, first: int = 0):
+    """Recipe D1: returns (prefix uint16[N][stride], depth int32[N]) — nodes
+    first .. first+N-1 of the seeded pool (a shard of a larger pool)."""
+    rows = np.arange(first, first + N)
     depth = (_draw(seed, 0, rows) % np.uint64(n)).astype(np.int32)
-    return random_prefixes(n, depth, seed, stride), depth
+    return random_prefixes(n, depth, seed, stride, first), depth
 
 
 def pool_fixed_depth(n: int, N: int, d: int, seed: int, stride: int | None = None):

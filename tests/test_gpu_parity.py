@@ -252,3 +252,75 @@ def test_parity_walk16_offset_boundary(torch, fsp, orc, n, m):
         pf, dp = inputs.pool_d1(n, 3000, 4242 + pmax)
         inst = compare(torch, fsp, orc, ptm, pf, dp)
         assert inst.info["walk16"] == walk16
+
+
+# ------------------------------------------- bench launch shapes
+
+def _sampled(torch, fsp, orc, ptm, pf, dp, k, seed):
+    inst = fsp.Instance(ptm)
+    got = gpu_lb(torch, inst, pf, dp)
+    assert inst.check() == fsp.FSP_OK
+    N = len(dp)
+    rng = np.random.default_rng(seed)
+    sample = np.concatenate([rng.choice(N - 200, k, replace=False), np.arange(N - 200, N)])
+    want = orc.Tables(ptm).lb_eval(pf[sample], dp[sample])
+    bad = np.nonzero(got[sample] != want)[0]
+    assert bad.size == 0, (sample[bad[:5]], got[sample][bad[:5]], want[bad[:5]])
+    return inst, got
+
+
+def test_full_size_500x20_bench_shape(torch, fsp, orc):
+    """BASELINE configs[4] (ta111-class 500x20) at a 262,144-node D1 pool plus a
+    ragged tail of 77 nodes: the launch shape is the bench one (no couple
+    split, several tile iterations per CTA, every couple group cycling through
+    the TMA buffers), checked on 3,000 random nodes and the last 200."""
+    n, m, seed = inputs.TAILLARD_SEEDS["ta111"]
+    ptm = inputs.taillard(n, m, seed)
+    N = (1 << 18) + 77
+    pf, dp = inputs.pool_d1(n, N, inputs.pool_seed("ta111"))
+    inst = fsp.Instance(ptm)
+    li = inst.launch_info(N)
+    assert li["split"] == 1 and li["iterations"] > 1 and li["groups"] > li["group_buffers"]
+    _, got = _sampled(torch, fsp, orc, ptm, pf, dp, 3000, 11)
+    assert got.min() >= int(ptm.sum(0).max()) and got.max() <= (n + m - 1) * int(ptm.max())
+
+
+def test_full_size_50x20_4m_sampled(torch, fsp, orc):
+    """BASELINE configs[2] (ta051-class 50x20) at the top of its pool sweep,
+    4,194,304 nodes, bench launch shape, sampled."""
+    n, m, seed = inputs.TAILLARD_SEEDS["ta051"]
+    ptm = inputs.taillard(n, m, seed)
+    N = 1 << 22
+    pf, dp = inputs.pool_d1(n, N, inputs.pool_seed("ta051"))
+    inst = fsp.Instance(ptm)
+    li = inst.launch_info(N)
+    assert li["split"] == 1 and li["iterations"] > 1
+    _sampled(torch, fsp, orc, ptm, pf, dp, 4000, 12)
+
+
+def test_20x5_split1_every_node(torch, fsp, orc, monkeypatch):
+    """The m = 5 kernel (lane-major rows, several CTAs per SM) without the
+    couple split, on a 65,536-node ta001 pool: every LB against the oracle."""
+    monkeypatch.setenv("FSP_LB_SPLIT", "1")
+    n, m, seed = inputs.TAILLARD_SEEDS["ta001"]
+    ptm = inputs.taillard(n, m, seed)
+    N = 1 << 16
+    pf, dp = inputs.pool_d1(n, N, inputs.pool_seed("ta001") + 5)
+    inst = fsp.Instance(ptm)
+    li = inst.launch_info(N)
+    assert li["split"] == 1 and li["row_layout"] == 0
+    compare(torch, fsp, orc, ptm, pf, dp)
+    # and the bench-size 1M pool in the default shape, sampled
+    monkeypatch.delenv("FSP_LB_SPLIT")
+    pf, dp = inputs.pool_d1(n, 1 << 20, inputs.pool_seed("ta001"))
+    assert inst.launch_info(1 << 20)["split"] == 1
+    _sampled(torch, fsp, orc, ptm, pf, dp, 20000, 13)
+
+
+@pytest.mark.parametrize("name", ["ta021", "ta091"])
+def test_bench_shape_launch_info(fsp, name):
+    """The 1M-node bench pools run unsplit with several tile iterations."""
+    n, m, seed = inputs.TAILLARD_SEEDS[name]
+    inst = fsp.Instance(inputs.taillard(n, m, seed))
+    li = inst.launch_info(1 << 20)
+    assert li["split"] == 1 and li["iterations"] >= 2 and li["grid"] >= 148

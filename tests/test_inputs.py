@@ -32,3 +32,14 @@ def test_fixed_depth_pools():
         assert (dp == d).all()
         for i in range(64):
             assert sorted(set(pf[i, :d].tolist())) == sorted(pf[i, :d].tolist())
+
+
+def test_pool_d1_shards_concatenate():
+    # strong scaling (bench.py --strong-total): every rank generates only its
+    # shard [lo, hi) of one pool, and the shards concatenate to the pool
+    from paper_1208_3933_b200 import dist as fdist
+    full_pf, full_dp = inputs.pool_d1(37, 1001, 99)
+    parts = [inputs.pool_d1(37, hi - lo, 99, first=lo)
+             for lo, hi in (fdist.shard(1001, r, 3) for r in range(3))]
+    assert (np.concatenate([p[0] for p in parts]) == full_pf).all()
+    assert (np.concatenate([p[1] for p in parts]) == full_dp).all()
