@@ -94,6 +94,7 @@ typedef struct {
     int32_t tmem_cols;        /* TMEM columns per CTA (0: heads in smem)      */
     int32_t sparse_walk;      /* 1: walk over the block's live jobs only      */
     int32_t smem_bytes;
+    int32_t tail_split;       /* split of the last, partial tile iteration    */
 } fsp_lb_launch;
 
 int fsp_lb_launch_info(const fsp_instance *inst, int64_t pool, int32_t sibling,

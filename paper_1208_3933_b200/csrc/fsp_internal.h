@@ -94,6 +94,8 @@ int fsp_cuda_fail(cudaError_t e, const char *what);
 // lb kernel launch (lb_kernel.cu)
 int fsp_plan_lb(fsp_instance *inst, bool sparse);
 int fsp_lb_split(const fsp_lb_plan &pl, int64_t pool);
+int fsp_lb_tail_split(const fsp_lb_plan &pl, int64_t pool, int split);
+int64_t fsp_lb_tail_first(const fsp_lb_plan &pl, int64_t pool);
 int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                   const int32_t *depth, int64_t pool, int32_t *lb_out, cudaStream_t s);
 // same, pool size read on the device from *pool_dev when pool_dev != nullptr

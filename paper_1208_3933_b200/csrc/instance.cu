@@ -233,5 +233,6 @@ extern "C" int fsp_lb_launch_info(const fsp_instance *inst, int64_t pool, int32_
     out->tmem_cols = pl.tm_cols;
     out->sparse_walk = pl.sparse ? 1 : 0;
     out->smem_bytes = (int32_t)pl.smem_bytes;
+    out->tail_split = sibling ? 1 : fsp_lb_tail_split(pl, pool, split);
     return FSP_OK;
 }

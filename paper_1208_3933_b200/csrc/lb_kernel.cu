@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -57,17 +58,27 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
 
 // The waiting warp suspends in try_wait (time hint) instead of spinning: a
 // spin loop here took 9 % of the issue slots of the walk's SM (ncu v12).
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, uint32_t hint_ns = 1000000u)
 {
     uint32_t done = 0;
     while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
-            : "memory");
+        if (hint_ns) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
+                : "memory");
+        } else {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(smem_u32(bar)), "r"(parity)
+                : "memory");
+        }
     }
 }
 
@@ -178,7 +189,16 @@ struct LbArgs {
     int woff;              // 16-bit walk offset D (= max p): e + D is carried
     int split;             // warps per tile (power of two <= W): each walks every
                            // split-th couple, LBs combined by atomicMax (lb_out zeroed)
+    int tail_split;        // split of the last (partial) tile iteration (1: none);
+                           // its nodes' lb_out entries are zeroed by the host
+    unsigned long long *prof; // diagnostics (FSP_LB_PROF): per-phase SM cycles, summed
+    uint32_t wait_ns;      // mbarrier try_wait suspend-time hint (0: none)
+    int dbg_skip;          // diagnostics only (FSP_LB_DEBUG_SKIP): bit 0 skips the
+                           // per-node heads phase, bit 1 the couple walks (LBs wrong)
 };
+
+// FSP_LB_PROF phases: cycles lane 0 of every warp spends in each part
+enum { PR_INGEST = 0, PR_HEADS, PR_WAIT, PR_WALK, PR_RELEASE, PR_STORE, PR_N };
 
 // Shared address of U[job][warp] from a record's meta word (wst = 4*NPL*warp).
 //   int32 form: meta = (c2 << 16) | addr    -> (meta & 0xffff) | wst  (one LOP3)
@@ -362,8 +382,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
     // small pools (fewer tiles than warps on the GPU): `split` warps share a
     // tile, each walking every split-th couple of a group (phase A is repeated
     // per warp); warps split*t .. split*t+split-1 sit on different SMSPs
-    const int split = a.split, slice = warp & (split - 1);
-    const int Wt = W / split; // tiles per CTA iteration
+    const int Wt = W / a.split; // tiles per CTA iteration
     const long long niter = (ntiles + (long long)Wt * gridDim.x - 1) / ((long long)Wt * gridDim.x);
     // double-buffered couple groups: the CTA's sequence of groups is it*G + gi;
     // group sequence number sq lives in buffer sq % NB, whose (sq / NB)-th fill
@@ -424,8 +443,20 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
     const uint64_t wst64 = (uint64_t)wst << 32;
     const int useg = UL::NIB ? 0 : WPR * warp; // this warp's segment of a U row
 
+    long long pt = a.prof ? clock64() : 0;
+    auto mark = [&](int ph) {
+        if (a.prof) {
+            const long long t = clock64();
+            if (lane == 0) atomicAdd(&a.prof[ph], (unsigned long long)(t - pt));
+            pt = t;
+        }
+    };
     for (long long it = 0; it < niter; ++it) {
-        const long long tile = (it * Wt + warp / split) * gridDim.x + blockIdx.x;
+        // the last, partial iteration may split its tiles over more warps (a
+        // partial wave otherwise leaves most warps of every SM idle)
+        const int split = it + 1 == niter && a.tail_split > a.split ? a.tail_split : a.split;
+        const int slice = warp & (split - 1);
+        const long long tile = it * Wt * gridDim.x + (long long)(warp / split) * gridDim.x + blockIdx.x;
         bool bad = false;
 
         // ---------------- a1: node ingest (depth, scheduled set) ----------------
@@ -553,9 +584,10 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             }
         }
 
+        mark(PR_INGEST);
         // ---------------- per node of this lane: C, heads, tails ----------------
 #pragma unroll 1
-        for (int q = 0; q < NPL; ++q) {
+        for (int q = 0; q < ((a.dbg_skip & 1) ? 0 : NPL); ++q) {
             const long long node = tile * TN + q * 32 + lane;
             int d = dq[0]; // (select chain: no local-memory indexing)
 #pragma unroll
@@ -764,6 +796,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
         if (bad) atomicOr(a.err, 1);
         if constexpr (TM) tm_wait_st();
         __syncwarp();
+        mark(PR_HEADS);
 
         // ---------------- a4/a5: couple walks (Fig. 3 lines 03-19) ----------------
         int lb[NPL]; // R1: the max over couples starts at 0
@@ -777,9 +810,10 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             const int g = dbuf ? gi : ascending ? gi : a.groups - 1 - gi;
             const long long sq = it * a.groups + gi;
             const uint8_t *tab = s_tab;
+            mark(PR_WALK);
             if (dbuf) { // wait for this group's buffer; no CTA-wide barrier
                 const int b = (int)(sq % NB);
-                mbar_wait(s_bar + b, (uint32_t)((sq / NB) & 1));
+                mbar_wait(s_bar + b, (uint32_t)((sq / NB) & 1), a.wait_ns);
                 tab = s_tab + (size_t)b * a.L.group_bytes;
             } else if (g != resident) {
                 __syncthreads(); // every warp is done with the resident group
@@ -793,12 +827,13 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 phase ^= 1;
                 resident = g;
             }
+            mark(PR_WAIT);
             if (anyvalid != 0) {
             const uint32_t *kl = reinterpret_cast<const uint32_t *>(tab);
             const uint4 *recs = reinterpret_cast<const uint4 *>(tab + a.L.kl_bytes);
             const int np = group_size(g);
             const int n2 = a.nrec >> 1, n4 = a.nrec >> 2;
-            for (int pl = slice; pl < np; pl += split) {
+            for (int pl = slice; pl < ((a.dbg_skip & 2) ? 0 : np); pl += split) {
                 const uint32_t kv = kl[pl];
                 const int k = kv & 0xffff, l = kv >> 16;
                 // lines 06-07: timeOnM1 / timeOnM2 start at the RM minima, so
@@ -955,6 +990,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                     if (compact) __syncwarp(); // the next couple rewrites s_list
             }
             } // anyvalid
+            mark(PR_WALK);
             if (dbuf) {
                 // release the buffer; the last of the W warps (its (sq>>1)-th
                 // round of W arrivals completes) refills it with group sq + 2
@@ -977,6 +1013,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                     }
                 }
             }
+            mark(PR_RELEASE);
         }
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
@@ -987,7 +1024,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             }
         }
         __syncwarp();
+        mark(PR_STORE);
     }
+
     if constexpr (TM) { // every warp is done with its columns
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
@@ -1264,6 +1303,33 @@ int fsp_lb_split(const fsp_lb_plan &pl, int64_t pool)
     return split;
 }
 
+// First node of the last tile iteration of an unsplit launch.
+int64_t fsp_lb_tail_first(const fsp_lb_plan &pl, int64_t pool)
+{
+    const int64_t tn = 32 * pl.npl, tiles = (pool + tn - 1) / tn;
+    const int64_t slots = (int64_t)pl.grid * pl.warps;
+    const int64_t niter = (tiles + slots - 1) / slots;
+    return niter > 0 ? (niter - 1) * slots * tn : 0;
+}
+
+// Split of the last tile iteration of an unsplit launch: the tiles left for
+// it are spread over up to all warp slots (couple split, atomicMax combine).
+int fsp_lb_tail_split(const fsp_lb_plan &pl, int64_t pool, int split)
+{
+    // measured on 200x20 1M pools: the idle warps of the partial wave were the
+    // whole 8 % "wait" share, but splitting their tiles (repeated phase A) did
+    // not shorten the launch (5.80 vs 5.82 ms): off unless FSP_LB_TAIL=1
+    if (split != 1 || pool <= 0) return 1;
+    if (!getenv("FSP_LB_TAIL") || atoi(getenv("FSP_LB_TAIL")) == 0) return 1;
+    const int64_t tn = 32 * pl.npl, tiles = (pool + tn - 1) / tn;
+    const int64_t slots = (int64_t)pl.grid * pl.warps;
+    const int64_t rem = tiles - (fsp_lb_tail_first(pl, pool) / tn);
+    int s = 1;
+    while (s < pl.warps && rem * s * 2 <= slots) s *= 2;
+    while (pl.warps % s) s /= 2;
+    return s;
+}
+
 int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                   const int32_t *depth, int64_t pool, int32_t *lb_out, cudaStream_t s)
 {
@@ -1306,9 +1372,36 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.dbuf = pl.dbuf;
     a.woff = inst->max_p;
     a.split = fsp_lb_split(pl, pool);
+    a.tail_split = pool_dev ? 1 : fsp_lb_tail_split(pl, pool, a.split);
+    a.wait_ns = getenv("FSP_LB_WAIT_NS") ? (uint32_t)atol(getenv("FSP_LB_WAIT_NS")) : 1000000u;
+    a.dbg_skip = getenv("FSP_LB_DEBUG_SKIP") ? atoi(getenv("FSP_LB_DEBUG_SKIP")) : 0;
+    a.prof = nullptr;
+    static unsigned long long *prof_buf = nullptr; // diagnostics only (FSP_LB_PROF=1)
+    const bool prof = getenv("FSP_LB_PROF") && atoi(getenv("FSP_LB_PROF")) != 0;
+    if (prof) {
+        if (!prof_buf && cudaMalloc(&prof_buf, 8 * PR_N) != cudaSuccess) prof_buf = nullptr;
+        if (prof_buf) cudaMemsetAsync(prof_buf, 0, 8 * PR_N, s);
+        a.prof = prof_buf;
+    }
     if (a.split > 1 && pool > 0) { // R1: every LB is a max starting at 0
         cudaError_t e = cudaMemsetAsync(lb_out, 0, sizeof(int32_t) * (size_t)pool, s);
         if (e != cudaSuccess) return fsp_cuda_fail(e, "lb_out clear");
+    } else if (a.tail_split > 1) { // only the last iteration's nodes are combined
+        const int64_t first = fsp_lb_tail_first(pl, pool);
+        cudaError_t e = cudaMemsetAsync(lb_out + first, 0, sizeof(int32_t) * (size_t)(pool - first), s);
+        if (e != cudaSuccess) return fsp_cuda_fail(e, "lb_out clear");
     }
-    FSP_DISPATCH(launch, pl, a, s);
+    const int rc = [&]() -> int { FSP_DISPATCH(launch, pl, a, s); }();
+    if (prof && prof_buf && rc == FSP_OK) {
+        unsigned long long h[PR_N];
+        cudaMemcpyAsync(h, prof_buf, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        double tot = 0;
+        for (int i = 0; i < PR_N; ++i) tot += (double)h[i];
+        fprintf(stderr, "FSP_LB_PROF pool=%lld warps=%d split=%d: ingest %.1f%% heads %.1f%% wait %.1f%% "
+                        "walk %.1f%% release %.1f%% store %.1f%% (%.3g warp-cycles)\n",
+                (long long)pool, pl.warps, a.split, 100 * h[0] / tot, 100 * h[1] / tot, 100 * h[2] / tot,
+                100 * h[3] / tot, 100 * h[4] / tot, 100 * h[5] / tot, tot);
+    }
+    return rc;
 }

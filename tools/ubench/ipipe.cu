@@ -10,6 +10,7 @@
 // Output: one line per variant: warp-instructions of the measured op per
 // cycle per SMSP (1.0 = one per clock = the issue limit; 0.5 = a half-rate
 // pipe), plus the same as lane-ops/clk/SM.
+#include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
 #include <climits>
@@ -28,6 +29,9 @@ __global__ void __launch_bounds__(512) k(unsigned *out, unsigned x, unsigned y, 
 #pragma unroll
     for (int i = 0; i < 8; ++i) e[i] = threadIdx.x * (i + 1);
     unsigned pm = threadIdx.x * 2654435761u;
+    // operands in registers (a kernel parameter used under a predicate is
+    // otherwise re-read from the constant bank inside the predicated block)
+    unsigned yr = y ^ *(volatile unsigned *)&out[0], xr = x ^ *(volatile unsigned *)&out[1];
     __syncthreads();
     long long c0 = clock64();
 #pragma unroll 1
@@ -50,6 +54,36 @@ __global__ void __launch_bounds__(512) k(unsigned *out, unsigned x, unsigned y, 
             }
             if constexpr (V == 9) e[i] = __vimax3_u16x2(e[i], x, y);                  // VIMNMX3.U16x2
         }
+        if constexpr (V == 12) {
+            // six chains per mask word: one R2P sets P1..P6
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t nb = __umulhi(pm + (uint32_t)it, 0x9E3779B9u + 77u * i);
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                    if (nb & (2u << q)) {
+                        asm volatile("");
+                        e[q] = __viaddmax_u16x2(e[q], xr + i, yr);
+                    }
+                }
+            }
+        }
+        if constexpr (V == 10 || V == 11) {
+            // the walk's mix: per position a mask word from the FMA pipe
+            // (IMAD.HI), R2P into P1..P4, four predicated VIADDMNMX.U16x2 on
+            // four chains (V == 11: the same without predicates)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t nb = __umulhi(pm + (uint32_t)it, 0x9E3779B9u + 77u * i);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (V == 11 || (nb & (2u << q))) {
+                        asm volatile("");
+                        e[q] = __viaddmax_u16x2(e[q], xr + i, yr);
+                    }
+                }
+            }
+        }
         if constexpr (V == 7) pm = (pm ^ (pm >> 7)) + e[0];
         x += 3;
     }
@@ -69,9 +103,9 @@ __global__ void __launch_bounds__(512) k(unsigned *out, unsigned x, unsigned y, 
 }
 
 template <int V>
-void run(const char *name, const char *pipe, unsigned *d, int sms)
+void run(const char *name, const char *pipe, unsigned *d, int sms, int ctas_per_sm = 4)
 {
-    const int iters = 1 << 16, threads = 512, blocks = sms * 4;
+    const int iters = 1 << 16, threads = 512, blocks = sms * ctas_per_sm;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -100,7 +134,7 @@ void run(const char *name, const char *pipe, unsigned *d, int sms)
     for (int s = 0; s < sms; ++s) {
         if (!cnt[s]) continue;
         const double w = (double)(hi[s] - lo[s]);
-        rate += (double)cnt[s] * threads / 32 * iters * 8 / (4 * w);
+        rate += (double)cnt[s] * threads / 32 * iters * (V == 12 ? 48 : V >= 10 ? 32 : 8) / (4 * w);
         win += w;
         ++used;
     }
@@ -132,5 +166,15 @@ int main()
     run<5>("LOP3", "alu", d, sms);
     run<6>("IMAD.HI+IADD3", "fma", d, sms);
     run<8>("VIADDMNMX.U16x2|IMAD.HI", "mix", d, sms);
+    // walk mix: the rate printed counts the VIADDMNMX.U16x2 only (32 per
+    // iteration: 8 positions x 4 chains), next to 8 R2P and 8 IMAD.HI
+    run<10>("walk: R2P + 4 @P VIADDMNMX", "mix", d, sms);
+    run<11>("walk without predicates", "mix", d, sms);
+    // 4 warps per SMSP (one 512-thread CTA per SM), as the lb kernel runs
+    run<10>("walk R2P, 4 warps/SMSP", "mix", d, sms, 1);
+    run<11>("walk no pred, 4 warps/SMSP", "mix", d, sms, 1);
+    run<0>("VIADDMNMX.U16x2 4w/SMSP", "alu", d, sms, 1);
+    run<12>("walk 6 chains per R2P", "mix", d, sms);
+    run<12>("walk 6 chains, 4w/SMSP", "mix", d, sms, 1);
     return 0;
 }
