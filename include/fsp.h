@@ -138,11 +138,16 @@ int fsp_lb_eval_sibling(const fsp_instance *inst, const uint16_t *prefix, int32_
                         int32_t *lb_out, void *cuda_stream);
 
 /* fsp_lb_eval_host — same result with HOST buffers (the paper's offload
- * round trip): copies the pool to the device in chunks, bounds each
- * chunk and copies the LBs back, overlapping the three on two streams.
- * Synchronous: returns when lb_out is filled.  Pinned host memory gives full
- * PCIe bandwidth; pageable memory works but slower.  Returns FSP_EBADNODE if
- * a malformed node was seen.  Errors: EINVAL, ENOMEM, ECUDA. */
+ * round trip).  When prefix, depth and lb_out are pinned
+ * (cudaHostAlloc / cudaHostRegister: device-mapped; stride a multiple of 8,
+ * prefix 16-byte aligned), a gather kernel on 8 SMs reads each node's depth
+ * and only its 2*depth prefix bytes over PCIe (zero-copy, 16-byte vectors)
+ * into device chunk buffers while the bounding kernel bounds the previous
+ * chunk on the other SMs; the LBs are copied back.  Otherwise whole rows are
+ * copied to the device in chunks, bounded and the LBs copied back, the three
+ * overlapped on two streams.  Synchronous: returns when
+ * lb_out is filled.  Returns FSP_EBADNODE if a malformed node was seen.
+ * Errors: EINVAL, ENOMEM, ECUDA. */
 int fsp_lb_eval_host(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                      const int32_t *depth, int64_t pool, int32_t *lb_out);
 

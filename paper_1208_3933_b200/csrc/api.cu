@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 #include <new>
@@ -91,6 +92,8 @@ struct HostCtx {
     uint16_t *d_pf[2] = {nullptr, nullptr};
     int32_t *d_dp[2] = {nullptr, nullptr};
     int32_t *d_lb[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};      // gather of buffer s done
+    cudaEvent_t ev_done[2] = {nullptr, nullptr}; // bounding + D2H of buffer s done
 };
 
 void fsp_host_ctx_free(void *p)
@@ -102,10 +105,126 @@ void fsp_host_ctx_free(void *p)
         cudaFree(c->d_dp[s]);
         cudaFree(c->d_lb[s]);
     }
+    for (int s = 0; s < 2; ++s) {
+        if (c->ev[s]) cudaEventDestroy(c->ev[s]);
+        if (c->ev_done[s]) cudaEventDestroy(c->ev_done[s]);
+    }
     delete c;
 }
 
 static std::mutex g_ctx_mu;
+
+// Device address of a pinned, mapped host buffer (nullptr: pageable or not
+// host memory).
+template <typename T>
+static T *device_view(T *p)
+{
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+    return static_cast<T *>(at.devicePointer);
+}
+
+// One warp per 8 rows in flight: depths first (lanes 0..7), then each row's
+// 16-byte vectors holding prefix entries < depth (coalesced per row).
+__global__ void __launch_bounds__(1024) gather_rows_kernel(const uint16_t *__restrict__ h_pf, int stride,
+                                                           const int32_t *__restrict__ h_dp, int64_t cnt,
+                                                           uint16_t *d_pf, int32_t *d_dp)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int s8 = stride >> 3;
+    for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 8; r0 < cnt;
+         r0 += warps * 8) {
+        int dl = 0;
+        if (lane < 8 && r0 + lane < cnt) {
+            dl = h_dp[r0 + lane];
+            d_dp[r0 + lane] = dl;
+        }
+        int d8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int du = __shfl_sync(0xffffffffu, dl, u);
+            d8[u] = du > 0 ? (min(du, stride) + 7) >> 3 : 0; // a bad depth is the kernel's to flag
+        }
+        for (int cc = lane; cc < s8; cc += 32) {
+            uint4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (cc < d8[u]) v[u] = reinterpret_cast<const uint4 *>(h_pf + (size_t)(r0 + u) * stride)[cc];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (cc < d8[u]) reinterpret_cast<uint4 *>(d_pf + (size_t)(r0 + u) * stride)[cc] = v[u];
+        }
+    }
+}
+
+static int eval_host_gather(const fsp_instance *inst, HostCtx *c, const uint16_t *hp, int32_t stride,
+                            const int32_t *hd, int64_t pool, int32_t *lb_out)
+{
+    const fsp_lb_plan &pl = inst->plan;
+    const int gather_sms = 8; // 8 SMs move ~2d bytes/node at PCIe rate (measured: enough)
+    const int lb_grid = std::max(1, pl.num_sms - gather_sms) * pl.ctas_per_sm;
+    const int64_t tile = 32 * pl.npl;
+    int64_t chunk = std::min<int64_t>(1 << 18, std::max<int64_t>(1 << 15, (pool + 7) / 8));
+    chunk = (chunk + tile - 1) / tile * tile;
+    if (chunk > pool) chunk = pool;
+    if (c->cap_nodes < chunk || c->cap_stride < stride) {
+        for (int s = 0; s < 2; ++s) {
+            cudaFree(c->d_pf[s]);
+            cudaFree(c->d_dp[s]);
+            cudaFree(c->d_lb[s]);
+            c->d_pf[s] = nullptr;
+            c->d_dp[s] = nullptr;
+            c->d_lb[s] = nullptr;
+        }
+        c->cap_nodes = 0;
+        for (int s = 0; s < 2; ++s) {
+            cudaError_t e = cudaMalloc(&c->d_pf[s], sizeof(uint16_t) * (size_t)chunk * stride);
+            if (e == cudaSuccess) e = cudaMalloc(&c->d_dp[s], sizeof(int32_t) * (size_t)chunk);
+            if (e == cudaSuccess) e = cudaMalloc(&c->d_lb[s], sizeof(int32_t) * (size_t)chunk);
+            if (e != cudaSuccess) return fsp_cuda_fail(e, "staging allocation");
+        }
+        c->cap_nodes = chunk;
+        c->cap_stride = stride;
+    }
+    if (!c->ev[0]) {
+        for (int s = 0; s < 2; ++s) {
+            cudaError_t e = cudaEventCreateWithFlags(&c->ev[s], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done[s], cudaEventDisableTiming);
+            if (e != cudaSuccess) return fsp_cuda_fail(e, "event create");
+        }
+    }
+    cudaStream_t gs = c->st[1], ls = c->st[0];
+    const int64_t nchunks = (pool + chunk - 1) / chunk;
+    for (int64_t q = 0; q < nchunks; ++q) {
+        const int s = (int)(q & 1);
+        const int64_t off = q * chunk, cnt = std::min(chunk, pool - off);
+        cudaError_t e = cudaSuccess;
+        if (q >= 2) e = cudaStreamWaitEvent(gs, c->ev_done[s], 0); // buffer s is free again
+        if (e == cudaSuccess) {
+            gather_rows_kernel<<<gather_sms, 1024, 0, gs>>>(hp + (size_t)off * stride, stride, hd + off, cnt,
+                                                            c->d_pf[s], c->d_dp[s]);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev[s], gs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ls, c->ev[s], 0);
+        if (e != cudaSuccess) return fsp_cuda_fail(e, "gather");
+        int rc = fsp_launch_lb_dev(inst, c->d_pf[s], stride, c->d_dp[s], cnt, nullptr, nullptr, 0, false,
+                                   c->d_lb[s], ls, lb_grid);
+        if (rc != FSP_OK) return rc;
+        e = cudaMemcpyAsync(lb_out + off, c->d_lb[s], sizeof(int32_t) * (size_t)cnt, cudaMemcpyDeviceToHost, ls);
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_done[s], ls);
+        if (e != cudaSuccess) return fsp_cuda_fail(e, "D2H");
+    }
+    cudaError_t e = cudaStreamSynchronize(ls);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(gs);
+    if (e != cudaSuccess) return fsp_cuda_fail(e, "sync");
+    return fsp_check(inst, ls);
+}
 
 extern "C" int fsp_lb_eval_host(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                                 const int32_t *depth, int64_t pool, int32_t *lb_out)
@@ -130,6 +249,17 @@ extern "C" int fsp_lb_eval_host(const fsp_instance *inst, const uint16_t *prefix
     }
     HostCtx *c = static_cast<HostCtx *>(mi->host_ctx);
     std::lock_guard<std::mutex> g(c->mu);
+
+    // Zero-copy gather (the offload round trip of P:286-288 without the row
+    // padding): when the three buffers are pinned and device-mapped, a small
+    // gather kernel on a few SMs reads each node's depth and only its 2*depth
+    // prefix bytes over PCIe into the device chunk buffers while the bounding
+    // kernel, on the other SMs, bounds the previous chunk; LBs go back by copy.
+    const uint16_t *hp = device_view(prefix);
+    const int32_t *hd = device_view(depth);
+    if (hp && hd && device_view(lb_out) && stride % 8 == 0 &&
+        (reinterpret_cast<uintptr_t>(hp) & 15) == 0 && !getenv("FSP_HOST_COPY"))
+        return eval_host_gather(inst, c, hp, stride, hd, pool, lb_out);
 
     // chunk: about an eighth of the pool (2^16 .. 2^20 nodes, whole warp tiles),
     // so the copies of chunk i+1 overlap the kernel of chunk i and the first

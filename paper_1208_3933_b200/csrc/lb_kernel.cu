@@ -1333,15 +1333,18 @@ int fsp_lb_tail_split(const fsp_lb_plan &pl, int64_t pool, int split)
 int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                   const int32_t *depth, int64_t pool, int32_t *lb_out, cudaStream_t s)
 {
-    return fsp_launch_lb_dev(inst, prefix, stride, depth, pool, nullptr, nullptr, 0, false, lb_out, s);
+    return fsp_launch_lb_dev(inst, prefix, stride, depth, pool, nullptr, nullptr, 0, false, lb_out, s,
+                             0);
 }
 
 int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                       const int32_t *depth, int64_t pool, const int64_t *pool_dev,
                       const int32_t *cin, int32_t cin_stride, bool sparse, int32_t *lb_out,
-                      cudaStream_t s)
+                      cudaStream_t s, int grid_limit)
 {
-    const fsp_lb_plan &pl = sparse ? inst->plan_bb : inst->plan;
+    fsp_lb_plan pl = sparse ? inst->plan_bb : inst->plan;
+    // host path: a few SMs are left to the PCIe gather kernel of the next chunk
+    if (grid_limit > 0 && grid_limit < pl.grid) pl.grid = grid_limit;
     const uint8_t *tables = sparse ? inst->d_tables_bb : inst->d_tables;
     LbArgs a;
     a.tables = tables;

@@ -324,3 +324,27 @@ def test_bench_shape_launch_info(fsp, name):
     inst = fsp.Instance(inputs.taillard(n, m, seed))
     li = inst.launch_info(1 << 20)
     assert li["split"] == 1 and li["iterations"] >= 2 and li["grid"] >= 148
+
+
+@pytest.mark.parametrize("name,N", [("ta091", 300_007), ("ta021", 70_001), ("ta111", 40_003)])
+def test_host_api_pinned_gather_path(torch, fsp, orc, monkeypatch, name, N):
+    """fsp_lb_eval_host on pinned buffers takes the zero-copy gather path
+    (only 2*depth prefix bytes cross PCIe, several chunks in flight); its LBs
+    equal the device path's, the copy path's and, sampled, the oracle's."""
+    n, m, seed = inputs.TAILLARD_SEEDS[name]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, N, 4321)
+    inst = fsp.Instance(ptm)
+    h_pf = torch.from_numpy(pf.view(np.int16)).pin_memory()
+    h_dp = torch.from_numpy(dp).pin_memory()
+    h_lb = torch.full((N,), -1, dtype=torch.int32).pin_memory()
+    inst.lb_eval_host_ptr(h_pf.data_ptr(), pf.shape[1], h_dp.data_ptr(), N, h_lb.data_ptr())
+    got = h_lb.numpy().copy()
+    assert (got == gpu_lb(torch, inst, pf, dp)).all()
+    monkeypatch.setenv("FSP_HOST_COPY", "1")
+    h_lb.fill_(-1)
+    inst.lb_eval_host_ptr(h_pf.data_ptr(), pf.shape[1], h_dp.data_ptr(), N, h_lb.data_ptr())
+    assert (h_lb.numpy() == got).all()
+    rng = np.random.default_rng(5)
+    sample = np.concatenate([rng.choice(N, 800, replace=False), np.arange(N - 50, N)])
+    assert (got[sample] == orc.Tables(ptm).lb_eval(pf[sample], dp[sample])).all()
