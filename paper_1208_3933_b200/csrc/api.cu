@@ -166,12 +166,18 @@ static int eval_host_gather(const fsp_instance *inst, HostCtx *c, const uint16_t
                             const int32_t *hd, int64_t pool, int32_t *lb_out)
 {
     const fsp_lb_plan &pl = inst->plan;
-    const int gather_sms = 8; // 8 SMs move ~2d bytes/node at PCIe rate (measured: enough)
+    const int gather_sms = getenv("FSP_GATHER_SMS") ? atoi(getenv("FSP_GATHER_SMS")) : 8;
     const int lb_grid = std::max(1, pl.num_sms - gather_sms) * pl.ctas_per_sm;
     const int64_t tile = 32 * pl.npl;
-    int64_t chunk = std::min<int64_t>(1 << 18, std::max<int64_t>(1 << 15, (pool + 7) / 8));
-    chunk = (chunk + tile - 1) / tile * tile;
-    if (chunk > pool) chunk = pool;
+    // chunks of one wave of tiles on the bounding SMs (no couple split); the
+    // first ones are a quarter and a half wave, so the bounding starts after a
+    // short gather that nothing overlaps
+    const int64_t wave = (int64_t)lb_grid * pl.warps * tile;
+    const int64_t chunk = getenv("FSP_HOST_CHUNK") ? atoll(getenv("FSP_HOST_CHUNK")) : wave;
+    const bool ramp = !getenv("FSP_HOST_NORAMP");
+    auto chunk_of = [&](int64_t q) {
+        return !ramp ? chunk : q == 0 ? std::max<int64_t>(tile, chunk / 4) : q == 1 ? std::max<int64_t>(tile, chunk / 2) : chunk;
+    };
     if (c->cap_nodes < chunk || c->cap_stride < stride) {
         for (int s = 0; s < 2; ++s) {
             cudaFree(c->d_pf[s]);
@@ -199,10 +205,10 @@ static int eval_host_gather(const fsp_instance *inst, HostCtx *c, const uint16_t
         }
     }
     cudaStream_t gs = c->st[1], ls = c->st[0];
-    const int64_t nchunks = (pool + chunk - 1) / chunk;
-    for (int64_t q = 0; q < nchunks; ++q) {
+    int64_t off = 0;
+    for (int64_t q = 0; off < pool; ++q) {
         const int s = (int)(q & 1);
-        const int64_t off = q * chunk, cnt = std::min(chunk, pool - off);
+        const int64_t cnt = std::min(chunk_of(q), pool - off);
         cudaError_t e = cudaSuccess;
         if (q >= 2) e = cudaStreamWaitEvent(gs, c->ev_done[s], 0); // buffer s is free again
         if (e == cudaSuccess) {
@@ -213,12 +219,16 @@ static int eval_host_gather(const fsp_instance *inst, HostCtx *c, const uint16_t
         if (e == cudaSuccess) e = cudaEventRecord(c->ev[s], gs);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(ls, c->ev[s], 0);
         if (e != cudaSuccess) return fsp_cuda_fail(e, "gather");
-        int rc = fsp_launch_lb_dev(inst, c->d_pf[s], stride, c->d_dp[s], cnt, nullptr, nullptr, 0, false,
-                                   c->d_lb[s], ls, lb_grid);
+        // (FSP_GATHER_ONLY: diagnostics, the transfers without the bounding)
+        int rc = getenv("FSP_GATHER_ONLY") ? FSP_OK
+                                           : fsp_launch_lb_dev(inst, c->d_pf[s], stride, c->d_dp[s], cnt,
+                                                               nullptr, nullptr, 0, false, c->d_lb[s], ls,
+                                                               lb_grid);
         if (rc != FSP_OK) return rc;
         e = cudaMemcpyAsync(lb_out + off, c->d_lb[s], sizeof(int32_t) * (size_t)cnt, cudaMemcpyDeviceToHost, ls);
         if (e == cudaSuccess) e = cudaEventRecord(c->ev_done[s], ls);
         if (e != cudaSuccess) return fsp_cuda_fail(e, "D2H");
+        off += cnt;
     }
     cudaError_t e = cudaStreamSynchronize(ls);
     if (e == cudaSuccess) e = cudaStreamSynchronize(gs);
