@@ -137,6 +137,25 @@ int fsp_lb_eval_sibling(const fsp_instance *inst, const uint16_t *prefix, int32_
                         const int32_t *depth, const int32_t *completion, int64_t pool,
                         int32_t *lb_out, void *cuda_stream);
 
+/* fsp_lb_eval_children — sibling-incremental bounding (SURVEY.md §8(f)
+ * NEXT-1): the LB of EVERY child of each parent (the parent's prefix + one
+ * unscheduled job j, forward branching P:138-140), from one forward and one
+ * backward pass per couple over the parent's unscheduled set (closed-form
+ * compositions of Fig. 3's per-job updates); bit-identical to
+ * fsp_lb_eval on the children.
+ *   prefix, stride, depth  DEVICE parents, layout as fsp_lb_eval; every parent
+ *                          must have 1 <= n - depth <= 32 (n <= 256).
+ *   completion             DEVICE int32 [n_parents][n_machines] parent C_k, or
+ *                          NULL (recomputed from the prefix).
+ *   lb_out                 DEVICE int32 [n_parents][32]: lb_out[p*32 + t] = LB
+ *                          of the child adding the t-th unscheduled job of
+ *                          parent p (ascending job id), t < n - depth[p];
+ *                          other entries are not written.
+ * Errors: EINVAL; ERANGE (n > 256: tables not built); ECUDA. */
+int fsp_lb_eval_children(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
+                         const int32_t *depth, const int32_t *completion, int64_t n_parents,
+                         int32_t *lb_out, void *cuda_stream);
+
 /* fsp_lb_eval_host — same result with HOST buffers (the paper's offload
  * round trip).  When prefix, depth and lb_out are pinned
  * (cudaHostAlloc / cudaHostRegister: device-mapped; stride a multiple of 8,

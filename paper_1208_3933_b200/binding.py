@@ -23,7 +23,7 @@ _NAMES = {0: "FSP_OK", -1: "FSP_EINVAL", -2: "FSP_ERANGE", -3: "FSP_ENOMEM", -4:
 # every symbol include/fsp.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "fsp_instance_load", "fsp_instance_free", "fsp_instance_get_info", "fsp_lb_launch_info",
-    "fsp_lb_eval",
+    "fsp_lb_eval", "fsp_lb_eval_children",
     "fsp_lb_eval_host", "fsp_lb_eval_sibling", "fsp_check", "fsp_lb_work", "fsp_bb_solve", "fsp_bb_init",
     "fsp_bb_step", "fsp_bb_ub_publish", "fsp_bb_ub_adopt", "fsp_bb_ub_get", "fsp_bb_ub_set",
     "fsp_bb_pool_size", "fsp_bb_node_bytes",
@@ -78,6 +78,7 @@ def lib():
             "fsp_lb_eval": (C.c_int, [vp, vp, i32, vp, i64, vp, vp]),
             "fsp_lb_eval_host": (C.c_int, [vp, vp, i32, vp, i64, vp]),
             "fsp_lb_eval_sibling": (C.c_int, [vp, vp, i32, vp, vp, i64, vp, vp]),
+            "fsp_lb_eval_children": (C.c_int, [vp, vp, i32, vp, vp, i64, vp, vp]),
             "fsp_check": (C.c_int, [vp, vp]),
             "fsp_lb_work": (i64, [i32, i32, i32]),
             "fsp_bb_solve": (C.c_int, [vp, i32, i64, C.c_double, C.POINTER(i32), vp,
@@ -190,6 +191,19 @@ class Instance:
         cp = _ptr(completion) if completion is not None else None
         _check(lib().fsp_lb_eval_sibling(self._h, _ptr(prefix), stride, _ptr(depth), cp, pool,
                                          _ptr(out), _stream(stream)))
+        return out
+
+    def lb_eval_children(self, prefix, depth, completion=None, out=None, stream=None):
+        """fsp_lb_eval_children on torch CUDA tensors: out int32 [parents][32],
+        out[p, t] = LB of parent p + its t-th unscheduled job (ascending)."""
+        import torch
+        B = depth.shape[0]
+        if out is None:
+            out = torch.full((B, 32), -1, dtype=torch.int32, device=depth.device)
+        stride = prefix.shape[1] if prefix.dim() == 2 else 1
+        cp = _ptr(completion) if completion is not None else None
+        _check(lib().fsp_lb_eval_children(self._h, _ptr(prefix), stride, _ptr(depth), cp, B,
+                                          _ptr(out), _stream(stream)))
         return out
 
     def lb_eval_host(self, prefix: np.ndarray, depth: np.ndarray, out=None):

@@ -68,6 +68,13 @@ struct fsp_lb_plan {
     size_t smem_bytes;   // dynamic smem per CTA
 };
 
+// Shared-memory tables of the sibling-incremental (family) kernel, family.cu.
+struct fsp_fam_layout {
+    size_t off_kl, off_pos, off_jm, off_pc, off_q, table_bytes; // per CTA
+    size_t warp_bytes;   // per-warp scratch
+    int warps;           // warps per CTA (0: family kernel unavailable)
+};
+
 struct fsp_instance {
     int n, m, P;
     int device;
@@ -83,9 +90,18 @@ struct fsp_instance {
     fsp_lb_plan plan;    // arbitrary pools (dense walk)
     fsp_lb_plan plan_bb; // B&B child pools (sparse walk, completion times supplied)
     uint8_t *d_tables_bb; // tables laid out for plan_bb
+    fsp_fam_layout fam;   // family kernel tables (n <= 256)
+    uint8_t *d_fam;
     // host-API staging (lazily created, guarded by a mutex in api.cu)
     void *host_ctx;
 };
+
+// family kernel (family.cu): LBs of parents' children by prefix/suffix
+// compositions; B&B mode (off/ckey) or every child (off == nullptr, out[p*32+t])
+int fsp_fam_build(fsp_instance *inst);
+int fsp_launch_family(const fsp_instance *inst, const uint16_t *ppf, int32_t stride, const int32_t *pdp,
+                      const int32_t *pC, int64_t B, const int64_t *off, const unsigned long long *ckey,
+                      int32_t *out, const int *flag, cudaStream_t s);
 
 // thread-local last error
 int fsp_fail(int code, const std::string &msg);

@@ -172,6 +172,11 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
         fsp_instance_free(inst);
         return fsp_cuda_fail(e, "instance upload");
     }
+    rc = fsp_fam_build(inst);
+    if (rc != FSP_OK) {
+        fsp_instance_free(inst);
+        return rc;
+    }
     *out = inst;
     return FSP_OK;
 }
@@ -187,6 +192,7 @@ extern "C" void fsp_instance_free(fsp_instance *inst)
     if (inst->d_ptm32s) cudaFree(inst->d_ptm32s);
     if (inst->d_ptm32) cudaFree(inst->d_ptm32);
     if (inst->d_err) cudaFree(inst->d_err);
+    if (inst->d_fam) cudaFree(inst->d_fam);
     delete[] inst->h_ptm;
     delete inst;
 }

@@ -348,3 +348,65 @@ def test_host_api_pinned_gather_path(torch, fsp, orc, monkeypatch, name, N):
     rng = np.random.default_rng(5)
     sample = np.concatenate([rng.choice(N, 800, replace=False), np.arange(N - 50, N)])
     assert (got[sample] == orc.Tables(ptm).lb_eval(pf[sample], dp[sample])).all()
+
+
+# ------------------------- sibling-incremental bounding (NEXT-1, family.cu)
+
+def _children_of(pf, dp, n):
+    """Every child (parent prefix + unscheduled j, ascending j) of each parent,
+    as rows + depths, with (parent, t) of each child (test-side enumeration)."""
+    rows, deps, where = [], [], []
+    for i in range(len(dp)):
+        d = int(dp[i])
+        used = set(int(x) for x in pf[i, :d])
+        t = 0
+        for j in range(n):
+            if j in used:
+                continue
+            r = pf[i].copy()
+            r[d] = j
+            rows.append(r)
+            deps.append(d + 1)
+            where.append((i, t))
+            t += 1
+    return np.stack(rows), np.array(deps, np.int32), where
+
+
+@pytest.mark.parametrize("name,nparents", [("ta001", 400), ("ta021", 300), ("ta051", 200),
+                                           ("ta091", 120)])
+def test_parity_children_family(torch, fsp, orc, name, nparents):
+    """fsp_lb_eval_children (prefix/suffix compositions per couple) equals the
+    oracle on every child of parents with 1..32 unscheduled jobs, with the
+    parents' completion times given and recomputed."""
+    n, m, seed = inputs.TAILLARD_SEEDS[name]
+    ptm = inputs.taillard(n, m, seed)
+    rng = np.random.default_rng(17)
+    depth = n - rng.integers(1, min(32, n) + 1, nparents)
+    pf = inputs.random_prefixes(n, depth.astype(np.int32), 77)
+    dp = depth.astype(np.int32)
+    inst = fsp.Instance(ptm)
+    rows, deps, where = _children_of(pf, dp, n)
+    want = orc.Tables(ptm).lb_eval(rows, deps)
+    C = torch.from_numpy(completion_times(ptm, pf, dp)).cuda()
+    for comp in (None, C):
+        got = inst.lb_eval_children(dev(torch, pf), dev(torch, dp), comp)
+        torch.cuda.synchronize()
+        got = got.cpu().numpy()
+        vals = np.array([got[i, t] for i, t in where])
+        bad = np.nonzero(vals != want)[0]
+        assert bad.size == 0, (name, comp is None, bad[:5], vals[bad[:5]], want[bad[:5]])
+
+
+@pytest.mark.parametrize("m", [2, 3, 7, 13, 25, 32])
+def test_parity_children_family_machine_counts(torch, fsp, orc, m):
+    rng = np.random.default_rng(100 + m)
+    n = int(rng.integers(2, 40))
+    ptm = rng.integers(0, 99, (n, m)).astype(np.int32)
+    depth = (n - rng.integers(1, min(32, n) + 1, 150)).astype(np.int32)
+    pf = inputs.random_prefixes(n, depth, 5)
+    inst = fsp.Instance(ptm)
+    rows, deps, where = _children_of(pf, depth, n)
+    want = orc.Tables(ptm).lb_eval(rows, deps)
+    got = inst.lb_eval_children(dev(torch, pf), dev(torch, depth)).cpu().numpy()
+    vals = np.array([got[i, t] for i, t in where])
+    assert (vals == want).all(), (m, n, int((vals != want).sum()))
