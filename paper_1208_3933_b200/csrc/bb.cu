@@ -68,6 +68,10 @@ struct BBState {
     Nodes st, kp, ch;     // stack, kept parents (scratch), children
     unsigned long long *ch_key; // per child: (idle << 12) | j (R19 tie key)
     int32_t *ord;         // child slot -> child record, siblings by descending (LB, key)
+    int32_t *d_maxnp;     // largest |S| among this iteration's expanded parents
+    int32_t *d_famflag;   // 1: the family kernel bounds this iteration's children
+    int64_t *d_count_sparse; // children for the lb kernel (0 when the family kernel runs)
+    bool family;          // sibling-incremental bounding enabled (n <= 256)
     long long *plan;      // per parent: (keep << 32) | children now
     int64_t *off;         // exclusive scan of plan; off[B] = (kept << 32) | children
     int64_t *d_count;     // children this iteration (LB pool size)
@@ -183,16 +187,17 @@ __global__ void scan_total_kernel(int64_t N, int64_t *out, const int64_t *tile_o
 // (at most K) and whether it stays open.  A parent whose LB (bounded when it
 // was a child) has reached the incumbent since is eliminated here (R9).
 __global__ void plan_kernel(Nodes st, int64_t first, int64_t B, int n, int K, const int32_t *inc_dev,
-                            long long *plan, unsigned long long *stats)
+                            long long *plan, unsigned long long *stats, int32_t *maxnp)
 {
     const int inc = *inc_dev;
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int dropped = 0;
+    int dropped = 0, np = 0;
     if (p < B) {
         const int64_t i = first + p;
         long long g = 0, keep = 0;
         if (st.lb[i] < inc) {
-            const int r = n - st.dp[i] - st.cur[i];
+            np = n - st.dp[i];
+            const int r = np - st.cur[i];
             g = r < K ? r : K;
             keep = r > g;
         } else {
@@ -200,8 +205,20 @@ __global__ void plan_kernel(Nodes st, int64_t first, int64_t B, int n, int K, co
         }
         plan[p] = (keep << 32) | g;
     }
+    np = __reduce_max_sync(0xffffffffu, (unsigned)np);
+    if ((threadIdx.x & 31) == 0 && np) atomicMax(maxnp, np);
     const unsigned b = __ballot_sync(0xffffffffu, dropped);
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(&stats[0], (unsigned long long)__popc(b));
+}
+
+// Bounding route: the family kernel (sibling-incremental, family.cu) when
+// every expanded parent has at most 32 unscheduled jobs, else the lb kernel.
+__global__ void route_kernel(const int32_t *maxnp, const int64_t *count, int family, int32_t *flag,
+                             int64_t *count_sparse)
+{
+    const int fam = family && *maxnp <= 32;
+    *flag = fam;
+    *count_sparse = fam ? 0 : *count;
 }
 
 // Branching (a7): one warp per parent; its unscheduled jobs of ascending
@@ -566,6 +583,9 @@ void bb_free(BBState *s)
     free_nodes(s->ch);
     cudaFree(s->ch_key);
     cudaFree(s->ord);
+    cudaFree(s->d_maxnp);
+    cudaFree(s->d_famflag);
+    cudaFree(s->d_count_sparse);
     cudaFree(s->plan);
     cudaFree(s->off);
     cudaFree(s->d_count);
@@ -729,21 +749,35 @@ int bb_iterate(BBState *s)
     const int64_t first = s->size - B;
 
     const int pb = 256;
-    plan_kernel<<<(unsigned)((B + pb - 1) / pb), pb, 0, st>>>(s->st, first, B, n, K, s->d_inc,
-                                                              s->plan, s->d_stats);
+    cudaError_t e0 = cudaMemsetAsync(s->d_maxnp, 0, 4, st);
+    if (e0 != cudaSuccess) return fsp_cuda_fail(e0, "B&B iteration");
+    plan_kernel<<<(unsigned)((B + pb - 1) / pb), pb, 0, st>>>(s->st, first, B, n, K, s->d_inc, s->plan,
+                                                              s->d_stats, s->d_maxnp);
     device_scan(s, s->plan, nullptr, B, s->off, s->d_count);
+    if (s->family)
+        route_kernel<<<1, 1, 0, st>>>(s->d_maxnp, s->d_count, 1, s->d_famflag, s->d_count_sparse);
     const int ewarps = n > 1024 ? 1 : 4;
     const int eblocks = (int)std::min<int64_t>((B + ewarps - 1) / ewarps, 148 * 32);
     const size_t esmem = (size_t)ewarps * 8 * (n + ((n + 31) / 32 + 1) / 2);
     expand_kernel<<<eblocks, ewarps * 32, esmem, st>>>(s->st, first, B, s->off, s->ch, s->ch_key,
                                                        s->kp, inst->d_ptm32, n, m, stride);
     const int64_t *off_B = s->off + B; // (kept << 32) | children, on the device
-    restore_kernel<<<eblocks, ewarps * 32, 0, st>>>(s->kp, off_B, first, s->st, m, stride);
-    // bounding: pool size read on the device, C from the parents, sparse walk
+    // bounding (before the kept parents overwrite the popped range): the
+    // family kernel from the parents (one of the two launches exits at once),
+    // or the lb kernel with the sparse-walk plan, pool size read on the device
+    // (the lb kernel first: a couple-split launch clears lb_out before it runs)
     const int64_t maxC = B * K;
-    int rc = fsp_launch_lb_dev(inst, s->ch.pf, stride, s->ch.dp, maxC, s->d_count, s->ch.C, m,
-                               s->sparse, s->ch.lb, st);
+    int rc = fsp_launch_lb_dev(inst, s->ch.pf, stride, s->ch.dp, maxC,
+                               s->family ? s->d_count_sparse : s->d_count, s->ch.C, m, s->sparse, s->ch.lb,
+                               st);
     if (rc != FSP_OK) return rc;
+    if (s->family) {
+        rc = fsp_launch_family(inst, s->st.pf + (size_t)first * stride, stride, s->st.dp + first,
+                               s->st.C + (size_t)first * m, B, s->off, s->ch_key, s->ch.lb, s->d_famflag,
+                               st);
+        if (rc != FSP_OK) return rc;
+    }
+    restore_kernel<<<eblocks, ewarps * 32, 0, st>>>(s->kp, off_B, first, s->st, m, stride);
     order_kernel<<<eblocks, ewarps * 32, 0, st>>>(s->ch.lb, s->ch_key, B, s->off, s->ord);
     const int nblk = (int)((maxC + kPruneThreads - 1) / kPruneThreads);
     prune_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->ord, s->d_count, n, s->d_inc, s->d_cand,
@@ -788,6 +822,10 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     // children per parent per pop: one lane per child in expand/order, K <= 32
     s->K = (int)std::min<int64_t>(32, std::max<int64_t>(1, env_i64("FSP_BB_K", 8)));
     s->dive_iters = std::max<int64_t>(0, env_i64("FSP_BB_DIVE", s->n));
+    // sibling-incremental bounding (family.cu) for batches of parents with <= 32
+    // unscheduled jobs: measured slower than the sparse walk at the B&B's
+    // depth mix, so opt-in (FSP_BB_FAMILY=1)
+    s->family = inst->fam.warps > 0 && env_i64("FSP_BB_FAMILY", 0) != 0;
     cudaError_t e = cudaSuccess;
     if (stream) {
         s->stream = static_cast<cudaStream_t>(stream);
@@ -816,6 +854,9 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     };
     alloc((void **)&s->ch_key, (size_t)s->ccap * 8);
     alloc((void **)&s->ord, (size_t)s->ccap * 4);
+    alloc((void **)&s->d_maxnp, 4);
+    alloc((void **)&s->d_famflag, 4);
+    alloc((void **)&s->d_count_sparse, 8);
     alloc((void **)&s->plan, (size_t)s->kcap * 8);
     alloc((void **)&s->off, (size_t)(s->kcap + 1) * 8);
     alloc((void **)&s->d_count, 8);

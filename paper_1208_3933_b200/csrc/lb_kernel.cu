@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
     lb_kernel(const LbArgs a)
 {
     extern __shared__ __align__(128) uint8_t smem[];
+    if (a.pool_dev && *a.pool_dev == 0) return; // B&B: an empty (or rerouted) pool
     const int n = a.n;
     const int m = EXACT ? MAXM : a.m;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

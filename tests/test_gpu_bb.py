@@ -279,3 +279,27 @@ def test_distributed_bb_world2_one_gpu_stealing(fsp, orc):
     assert all(o[2] == 0 and o[3] == opt for o in out), (out, opt)
     assert out[0][4] == out[1][4] and orc.makespan(p, out[0][4]) == opt
     assert out[0][5] > 0                        # work stealing moved nodes
+
+
+def test_bb_family_kernel_optima(fsp, orc, monkeypatch):
+    """The B&B with sibling-incremental bounding (FSP_BB_FAMILY=1: batches of
+    parents with <= 32 unscheduled jobs bounded by family.cu) reaches the same
+    optima; its child pools match the oracle element-wise."""
+    monkeypatch.setenv("FSP_BB_FAMILY", "1")
+    monkeypatch.setenv("FSP_BB_K", "32")
+    for name, opt in (("ta001", 1278), ("ta003", 1081)):
+        p = inputs.instance(name)
+        rc, ms, perm, _ = fsp.Instance(p).bb_solve(2**31 - 1, 0, 60.0)
+        assert rc == 0 and ms == opt and orc.makespan(p, perm) == opt
+    rng = np.random.default_rng(8)
+    for _ in range(4):
+        n, m = int(rng.integers(8, 12)), int(rng.integers(3, 6))
+        p = rng.integers(1, 99, (n, m)).astype(np.int32)
+        rc, ms, perm, _ = fsp.Instance(p).bb_solve()
+        assert rc == 0 and ms == orc.Tables(p).bb_dfs()[1] == orc.makespan(p, perm)
+    p = inputs.instance("ta021")
+    T = orc.Tables(p)
+    bb = fsp.BBState(fsp.Instance(p))
+    bb.step(40)
+    pf, dp, Cc, lb = bb.debug_children()
+    assert len(dp) > 0 and (T.lb_eval(pf, dp) == lb).all()
