@@ -208,6 +208,20 @@ int fsp_bb_solve(const fsp_instance *inst, int32_t initial_ub, int64_t max_nodes
                  double time_limit_s, int32_t *makespan_out, int32_t *perm_out,
                  fsp_bb_stats *stats);
 
+/* fsp_bb_solve_hybrid — multi-core host + GPU B&B (the paper's future work,
+ * P:607-609): `threads` host threads each drive their own device B&B state
+ * (own stream; thread 0 starts from the root, the others empty) on the
+ * current device, share the incumbent through a host
+ * atomic min (adopted after every step, R9) and steal work (an idle thread's
+ * request is answered with the donor's shallowest open nodes, moved device
+ * to device).  Every bound, branch and elimination runs in the device
+ * kernels; the host threads schedule.  Same result contract as fsp_bb_solve;
+ * stats are summed over the threads.  threads in [1, 64].
+ * Errors: EINVAL, ENOMEM, ECUDA, ENOTFOUND, EBUDGET. */
+int fsp_bb_solve_hybrid(const fsp_instance *inst, int32_t initial_ub, int32_t threads,
+                        int64_t max_nodes, double time_limit_s, int32_t *makespan_out,
+                        int32_t *perm_out, fsp_bb_stats *stats);
+
 /* Step-level B&B for the multi-GPU driver (torch.distributed owns the
  * collectives).  A state holds one device-resident pool.
  *  fsp_bb_init        state for rank/world (rank r keeps the root's

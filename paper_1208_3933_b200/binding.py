@@ -24,7 +24,7 @@ _NAMES = {0: "FSP_OK", -1: "FSP_EINVAL", -2: "FSP_ERANGE", -3: "FSP_ENOMEM", -4:
 EXPORTS = [
     "fsp_instance_load", "fsp_instance_free", "fsp_instance_get_info", "fsp_lb_launch_info",
     "fsp_lb_eval", "fsp_lb_eval_children",
-    "fsp_lb_eval_host", "fsp_lb_eval_sibling", "fsp_check", "fsp_lb_work", "fsp_bb_solve", "fsp_bb_init",
+    "fsp_lb_eval_host", "fsp_lb_eval_sibling", "fsp_check", "fsp_lb_work", "fsp_bb_solve", "fsp_bb_solve_hybrid", "fsp_bb_init",
     "fsp_bb_step", "fsp_bb_ub_publish", "fsp_bb_ub_adopt", "fsp_bb_ub_get", "fsp_bb_ub_set",
     "fsp_bb_pool_size", "fsp_bb_node_bytes",
     "fsp_bb_export", "fsp_bb_import", "fsp_bb_debug_children", "fsp_bb_result", "fsp_bb_get_stats",
@@ -83,6 +83,8 @@ def lib():
             "fsp_lb_work": (i64, [i32, i32, i32]),
             "fsp_bb_solve": (C.c_int, [vp, i32, i64, C.c_double, C.POINTER(i32), vp,
                                        C.POINTER(BBStats)]),
+            "fsp_bb_solve_hybrid": (C.c_int, [vp, i32, i32, i64, C.c_double, C.POINTER(i32), vp,
+                                              C.POINTER(BBStats)]),
             "fsp_bb_init": (C.c_int, [vp, i32, i32, i32, C.POINTER(vp)]),
             "fsp_bb_step": (C.c_int, [vp, i32, vp]),
             "fsp_bb_ub_publish": (C.c_int, [vp, vp, vp]),
@@ -235,6 +237,18 @@ class Instance:
         st = BBStats()
         rc = lib().fsp_bb_solve(self._h, int(initial_ub), int(max_nodes), float(time_limit_s),
                                 C.byref(ms), perm.ctypes.data, C.byref(st))
+        _check(rc, allow=(FSP_ENOTFOUND, FSP_EBUDGET))
+        return rc, int(ms.value), perm, {f: getattr(st, f) for f, _ in BBStats._fields_}
+
+    def bb_solve_hybrid(self, threads: int = 4, initial_ub: int = 2**31 - 1, max_nodes: int = 0,
+                        time_limit_s: float = 0.0):
+        """fsp_bb_solve_hybrid.  Returns (status, makespan, perm, stats)."""
+        ms = C.c_int32(0)
+        perm = np.zeros(self.n, np.int32)
+        st = BBStats()
+        rc = lib().fsp_bb_solve_hybrid(self._h, int(initial_ub), int(threads), int(max_nodes),
+                                       float(time_limit_s), C.byref(ms), perm.ctypes.data,
+                                       C.byref(st))
         _check(rc, allow=(FSP_ENOTFOUND, FSP_EBUDGET))
         return rc, int(ms.value), perm, {f: getattr(st, f) for f, _ in BBStats._fields_}
 

@@ -805,7 +805,8 @@ int bb_iterate(BBState *s)
 }
 
 int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_t world,
-              void *stream, BBState **out)
+              void *stream, BBState **out, double mem_frac = 0.0, int64_t children_cap = 0,
+              bool root_only = false)
 {
     if (!inst || !out || world < 1 || rank < 0 || rank >= world || initial_ub < 0)
         return fsp_fail(FSP_EINVAL, "bad B&B arguments");
@@ -837,10 +838,11 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     size_t freeb = 0, totalb = 0;
     if (e == cudaSuccess) e = cudaMemGetInfo(&freeb, &totalb);
     // children per iteration: enough to fill the GPU several times over
-    s->ccap = std::max<int64_t>(env_i64("FSP_BB_CHILDREN", 1 << 21), 32);
+    s->ccap = std::max<int64_t>(children_cap > 0 ? children_cap : env_i64("FSP_BB_CHILDREN", 1 << 21), 32);
     s->kcap = s->ccap;
     // the stack takes most of the free HBM (180 GB per B200)
-    const double frac = getenv("FSP_BB_MEM_FRAC") ? atof(getenv("FSP_BB_MEM_FRAC")) : 0.5;
+    const double frac = mem_frac > 0 ? mem_frac
+                        : getenv("FSP_BB_MEM_FRAC") ? atof(getenv("FSP_BB_MEM_FRAC")) : 0.5;
     const size_t buffers = (size_t)(s->ccap + s->kcap) * node_bytes(s);
     int64_t cap = freeb > buffers ? (int64_t)((double)(freeb - buffers) * frac / node_bytes(s)) : 0;
     cap = env_i64("FSP_BB_STACK", std::min<int64_t>(cap, (int64_t)1 << 31));
@@ -889,9 +891,10 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     // the depth-1 nodes j with j % world == r
     std::vector<uint16_t> pf;
     std::vector<int32_t> dp;
-    if (world == 1 || n == 1) {
+    if (world == 1 || n == 1 || root_only) {
         // (n == 1: the one depth-1 node is a complete schedule, which is only
-        // evaluated as a child; rank 0 starts from the root, the others empty)
+        // evaluated as a child; root_only: the other ranks get work by
+        // stealing; in both, rank 0 starts from the root, the others empty)
         if (rank == 0) {
             pf.assign(s->stride, 0xffff);
             dp.push_back(0);
@@ -968,6 +971,17 @@ extern "C" int fsp_bb_solve(const fsp_instance *inst, int32_t initial_ub, int64_
         if (budget) rc = fsp_fail(s->have ? FSP_EBUDGET : FSP_ENOTFOUND, "B&B budget exhausted");
     }
     bb_free(s);
+    return rc;
+}
+
+// (hybrid.cu: several states on one device share its memory)
+int fsp_bb_init_ex(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_t world,
+                   double mem_frac, int64_t children_cap, bool root_only, void **state)
+{
+    if (!state) return fsp_fail(FSP_EINVAL, "null state");
+    BBState *s = nullptr;
+    int rc = bb_create(inst, initial_ub, rank, world, nullptr, &s, mem_frac, children_cap, root_only);
+    *state = s;
     return rc;
 }
 

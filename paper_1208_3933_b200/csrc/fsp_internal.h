@@ -103,6 +103,11 @@ int fsp_launch_family(const fsp_instance *inst, const uint16_t *ppf, int32_t str
                       const int32_t *pC, int64_t B, const int64_t *off, const unsigned long long *ckey,
                       int32_t *out, const int *flag, cudaStream_t s);
 
+// B&B state with an explicit share of the free device memory and child
+// buffer size (hybrid.cu runs several on one device)
+int fsp_bb_init_ex(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_t world,
+                   double mem_frac, int64_t children_cap, bool root_only, void **state);
+
 // thread-local last error
 int fsp_fail(int code, const std::string &msg);
 int fsp_cuda_fail(cudaError_t e, const char *what);

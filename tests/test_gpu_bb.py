@@ -303,3 +303,29 @@ def test_bb_family_kernel_optima(fsp, orc, monkeypatch):
     bb.step(40)
     pf, dp, Cc, lb = bb.debug_children()
     assert len(dp) > 0 and (T.lb_eval(pf, dp) == lb).all()
+
+
+@pytest.mark.parametrize("threads", [2, 4])
+def test_bb_hybrid_threads(fsp, orc, threads):
+    """fsp_bb_solve_hybrid (host threads each driving a device B&B state,
+    shared incumbent, work stealing): the same optima as the oracle, the
+    ENOTFOUND proof below the optimum, budgets honoured."""
+    for name, opt in (("ta001", 1278), ("ta002", 1359), ("ta004", 1293)):
+        p = inputs.instance(name)
+        inst = fsp.Instance(p)
+        rc, ms, perm, st = inst.bb_solve_hybrid(threads, 2**31 - 1, 0, 120.0)
+        assert rc == 0 and ms == opt and orc.makespan(p, perm) == opt, (name, rc, ms)
+        assert sorted(perm.tolist()) == list(range(p.shape[0]))
+        rc, _, _, _ = inst.bb_solve_hybrid(threads, opt - 1, 0, 120.0)
+        assert rc == fsp.FSP_ENOTFOUND
+    rng = np.random.default_rng(threads)
+    for _ in range(6):
+        n, m = int(rng.integers(1, 11)), int(rng.integers(2, 6))
+        p = rng.integers(1, 60, (n, m)).astype(np.int32)
+        rc, ms, perm, _ = fsp.Instance(p).bb_solve_hybrid(threads)
+        assert rc == 0 and ms == orc.Tables(p).bb_dfs()[1] == orc.makespan(p, perm)
+    p = inputs.instance("ta021")
+    rc, ms, perm, st = fsp.Instance(p).bb_solve_hybrid(threads, 2**31 - 1, 2_000_000, 0.0)
+    assert rc in (fsp.FSP_EBUDGET, fsp.FSP_ENOTFOUND) and st["bounded"] >= 2_000_000
+    if rc == fsp.FSP_EBUDGET:
+        assert orc.makespan(p, perm) == ms

@@ -11,7 +11,12 @@ for arg in sys.argv[1:]:
     name, ub, secs = arg.split(":")
     p = inputs.instance(name)
     inst = binding.Instance(p)
-    rc, ms, perm, st = inst.bb_solve(int(ub), 0, float(secs))
+    threads = int(os.environ.get("BB_THREADS", "0"))
+    if threads:
+        rc, ms, perm, st = inst.bb_solve_hybrid(threads, int(ub), 0, float(secs))
+    else:
+        rc, ms, perm, st = inst.bb_solve(int(ub), 0, float(secs))
     st["nodes_per_s"] = st["bounded"] / max(st["wall_s"], 1e-9)
-    print(json.dumps({"instance": name, "initial_ub": int(ub), "rc": rc, "makespan": ms, **st}),
+    print(json.dumps({"instance": name, "threads": threads, "initial_ub": int(ub), "rc": rc,
+                      "makespan": ms, **st}),
           flush=True)
