@@ -258,7 +258,7 @@ def run_reference(a):
     print(json.dumps(out), flush=True)
 
 
-TABLE2_SIZES = [4096, 8192, 16384, 32768, 65536, 131072, 262144, 1048576]
+TABLE2_SIZES = [4096, 8192, 16384, 32768, 65536, 131072, 262144, 1048576, 4194304]
 TABLE2_CFGS = ["ta021", "ta051", "c100x20", "ta091"]
 
 
@@ -352,9 +352,13 @@ def run_table2(a):
             rows.append(row)
             if best is None or row["tcpu_over_tgpu_offload"] > best[1]:
                 best = (S, row["tcpu_over_tgpu_offload"])
+        # the runtime choice the paper asks for: fsp_lb_tune_pool
+        tuned, rates = inst.tune_pool(22, 0.95)
         print(json.dumps({"instance": f"{cfg}-class {n}x{m}", "best_pool_offload": best[0],
                           "best_tcpu_over_tgpu_offload": best[1], "bb_iterations_for_list":
-                          st.get("iterations")}), flush=True)
+                          st.get("iterations"), "runtime_pool_95pct": tuned,
+                          "tuned_rates_bounds_per_s": {str(k): v for k, v in rates.items()}}),
+              flush=True)
         inst.close()
     return rows
 

@@ -170,6 +170,17 @@ int fsp_lb_eval_children(const fsp_instance *inst, const uint16_t *prefix, int32
 int fsp_lb_eval_host(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                      const int32_t *depth, int64_t pool, int32_t *lb_out);
 
+/* fsp_lb_tune_pool — runtime pool-size choice (the paper: the pool size "has
+ * to be determined at runtime", §VI; Table II): times
+ * fsp_lb_eval on a synthetic D1-shaped pool generated on the device, for
+ * pool sizes 2^12 .. 2^max_log2 (12 <= max_log2 <= 24), and returns in
+ * *pool_out the smallest size whose bounds/s reach frac (0 < frac <= 1) of
+ * the best.  rates_out (HOST, nullable): max_log2 - 11 doubles, bounds/s per
+ * size.  Allocates (stream-ordered) and synchronises cuda_stream; not for
+ * the hot path.  Errors: EINVAL, ECUDA. */
+int fsp_lb_tune_pool(const fsp_instance *inst, int32_t max_log2, double frac, int64_t *pool_out,
+                     double *rates_out, void *cuda_stream);
+
 /* fsp_check — synchronises cuda_stream, then returns FSP_EBADNODE (and clears
  * the flag) if any bounding call on this instance saw a malformed node since
  * the last check, else FSP_OK. */

@@ -24,7 +24,7 @@ _NAMES = {0: "FSP_OK", -1: "FSP_EINVAL", -2: "FSP_ERANGE", -3: "FSP_ENOMEM", -4:
 EXPORTS = [
     "fsp_instance_load", "fsp_instance_free", "fsp_instance_get_info", "fsp_lb_launch_info",
     "fsp_lb_eval", "fsp_lb_eval_children",
-    "fsp_lb_eval_host", "fsp_lb_eval_sibling", "fsp_check", "fsp_lb_work", "fsp_bb_solve", "fsp_bb_solve_hybrid", "fsp_bb_init",
+    "fsp_lb_eval_host", "fsp_lb_eval_sibling", "fsp_check", "fsp_lb_tune_pool", "fsp_lb_work", "fsp_bb_solve", "fsp_bb_solve_hybrid", "fsp_bb_init",
     "fsp_bb_step", "fsp_bb_ub_publish", "fsp_bb_ub_adopt", "fsp_bb_ub_get", "fsp_bb_ub_set",
     "fsp_bb_pool_size", "fsp_bb_node_bytes",
     "fsp_bb_export", "fsp_bb_import", "fsp_bb_debug_children", "fsp_bb_result", "fsp_bb_get_stats",
@@ -80,6 +80,7 @@ def lib():
             "fsp_lb_eval_sibling": (C.c_int, [vp, vp, i32, vp, vp, i64, vp, vp]),
             "fsp_lb_eval_children": (C.c_int, [vp, vp, i32, vp, vp, i64, vp, vp]),
             "fsp_check": (C.c_int, [vp, vp]),
+            "fsp_lb_tune_pool": (C.c_int, [vp, i32, C.c_double, C.POINTER(i64), vp, vp]),
             "fsp_lb_work": (i64, [i32, i32, i32]),
             "fsp_bb_solve": (C.c_int, [vp, i32, i64, C.c_double, C.POINTER(i32), vp,
                                        C.POINTER(BBStats)]),
@@ -225,6 +226,14 @@ class Instance:
         """fsp_lb_eval_host on raw host pointers (e.g. pinned torch tensors)."""
         _check(lib().fsp_lb_eval_host(self._h, C.c_void_p(prefix_ptr), stride,
                                       C.c_void_p(depth_ptr), pool, C.c_void_p(out_ptr)))
+
+    def tune_pool(self, max_log2: int = 22, frac: float = 0.95, stream=None):
+        """fsp_lb_tune_pool: (chosen pool size, {size: bounds/s})."""
+        pool = C.c_int64(0)
+        rates = np.zeros(max_log2 - 11, np.float64)
+        _check(lib().fsp_lb_tune_pool(self._h, int(max_log2), float(frac), C.byref(pool),
+                                      rates.ctypes.data, _stream(stream)))
+        return int(pool.value), {1 << (12 + i): float(r) for i, r in enumerate(rates)}
 
     def check(self, stream=None) -> int:
         """fsp_check: FSP_OK or FSP_EBADNODE (raises on other errors)."""

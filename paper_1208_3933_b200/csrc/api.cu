@@ -7,6 +7,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "fsp_internal.h"
 
@@ -322,4 +323,101 @@ extern "C" int fsp_lb_eval_host(const fsp_instance *inst, const uint16_t *prefix
         if (e != cudaSuccess) return fsp_cuda_fail(e, "sync");
     }
     return fsp_check(inst, c->st[0]);
+}
+
+// ------------------------------------------------- runtime pool-size choice
+
+namespace {
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z)
+{
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Synthetic D1-shaped pool on the device (DESIGN.md §5 recipe, its own
+// counter-based stream): depth ~ U{0..n-1}, prefix = the first d entries of a
+// random permutation (partial Fisher-Yates in the row itself).
+__global__ void synth_pool_kernel(int n, int stride, int64_t N, unsigned long long seed, uint16_t *pf,
+                                  int32_t *dp)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        uint16_t *row = pf + (size_t)i * stride;
+        for (int j = 0; j < n; ++j) row[j] = (uint16_t)j;
+        const int d = (int)(mix64(seed ^ (unsigned long long)i * 0xD1B54A32D192ED03ull) % (unsigned)n);
+        for (int t = 0; t < d; ++t) {
+            const unsigned long long r = mix64(seed + 0x1234567ull * (t + 1) + (unsigned long long)i * 0x9E37ull);
+            const int u = t + (int)(r % (unsigned long long)(n - t));
+            const uint16_t a = row[t];
+            row[t] = row[u];
+            row[u] = a;
+        }
+        dp[i] = d;
+    }
+}
+
+} // namespace
+
+// The paper sets the pool size by hand and notes it "has to be determined at
+// runtime" (§VI; Table II): time the bounding kernel on
+// synthetic pools of 2^12 .. 2^max_log2 nodes and return the smallest size
+// whose throughput reaches `frac` of the best one.
+extern "C" int fsp_lb_tune_pool(const fsp_instance *inst, int32_t max_log2, double frac, int64_t *pool_out,
+                                double *rates_out, void *cuda_stream)
+{
+    if (!inst || !pool_out || max_log2 < 12 || max_log2 > 24 || !(frac > 0 && frac <= 1))
+        return fsp_fail(FSP_EINVAL, "bad tuning arguments");
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const int n = inst->n, stride = (n + 7) & ~7;
+    const int64_t Nmax = (int64_t)1 << max_log2;
+    uint16_t *pf = nullptr;
+    int32_t *dp = nullptr, *lb = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaError_t e = cudaMallocAsync(&pf, sizeof(uint16_t) * (size_t)Nmax * stride, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&dp, sizeof(int32_t) * (size_t)Nmax, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&lb, sizeof(int32_t) * (size_t)Nmax, s);
+    if (e == cudaSuccess) e = cudaEventCreate(&e0);
+    if (e == cudaSuccess) e = cudaEventCreate(&e1);
+    int rc = e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, "tuning buffers");
+    if (rc == FSP_OK) {
+        synth_pool_kernel<<<1184, 256, 0, s>>>(n, stride, Nmax, 12083933ull, pf, dp);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) rc = fsp_cuda_fail(e, "synthetic pool");
+    }
+    double best = 0;
+    std::vector<double> rate;
+    for (int lg = 12; lg <= max_log2 && rc == FSP_OK; ++lg) {
+        const int64_t N = (int64_t)1 << lg;
+        const int reps = (int)std::max<int64_t>(2, std::min<int64_t>(20, ((int64_t)1 << 22) / N));
+        rc = fsp_launch_lb(inst, pf, stride, dp, N, lb, s); // warm-up
+        if (rc == FSP_OK) e = cudaEventRecord(e0, s);
+        for (int r = 0; r < reps && rc == FSP_OK && e == cudaSuccess; ++r) rc = fsp_launch_lb(inst, pf, stride, dp, N, lb, s);
+        if (rc == FSP_OK && e == cudaSuccess) e = cudaEventRecord(e1, s);
+        if (rc == FSP_OK && e == cudaSuccess) e = cudaEventSynchronize(e1);
+        float ms = 0;
+        if (rc == FSP_OK && e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+        if (rc == FSP_OK && e != cudaSuccess) rc = fsp_cuda_fail(e, "tuning timing");
+        if (rc != FSP_OK) break;
+        const double r1 = (double)N * reps / (ms * 1e-3);
+        rate.push_back(r1);
+        if (rates_out) rates_out[lg - 12] = r1;
+        best = std::max(best, r1);
+    }
+    if (rc == FSP_OK) {
+        *pool_out = Nmax;
+        for (size_t i = 0; i < rate.size(); ++i)
+            if (rate[i] >= frac * best) {
+                *pool_out = (int64_t)1 << (12 + i);
+                break;
+            }
+    }
+    cudaFreeAsync(pf, s);
+    cudaFreeAsync(dp, s);
+    cudaFreeAsync(lb, s);
+    cudaStreamSynchronize(s);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    return rc;
 }

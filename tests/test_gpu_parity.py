@@ -410,3 +410,14 @@ def test_parity_children_family_machine_counts(torch, fsp, orc, m):
     got = inst.lb_eval_children(dev(torch, pf), dev(torch, depth)).cpu().numpy()
     vals = np.array([got[i, t] for i, t in where])
     assert (vals == want).all(), (m, n, int((vals != want).sum()))
+
+
+def test_tune_pool(torch, fsp):
+    """fsp_lb_tune_pool (runtime pool-size choice): a power of two
+    in range whose measured rate reaches the requested fraction of the best."""
+    n, m, seed = inputs.TAILLARD_SEEDS["ta021"]
+    inst = fsp.Instance(inputs.taillard(n, m, seed))
+    pool, rates = inst.tune_pool(18, 0.9)
+    assert pool in rates and all(r > 0 for r in rates.values())
+    assert rates[pool] >= 0.9 * max(rates.values())
+    assert all(rates[s] < 0.9 * max(rates.values()) for s in rates if s < pool)
