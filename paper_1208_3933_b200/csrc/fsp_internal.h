@@ -59,6 +59,7 @@ struct fsp_lb_plan {
     int pairs_per_group; // couples per group (last group may be shorter)
     int dbuf;            // couple-group buffers in shared memory (0: one + CTA barrier)
     bool byte_rows;      // 16-bit walk, m >= 10: U rows of one byte per lane (else nibbles)
+    bool recs_global;    // ablation: couple records read from global memory (20-machine dense)
     int warps;           // warps per CTA
     int ctas_per_sm;
     int num_sms;

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <string>
 #include <cstdlib>
 #include <type_traits>
 
@@ -313,7 +314,9 @@ __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1
 // launch bounds: 8 warps for m > 20; 4 warps x 5 CTAs per SM for m = 5 (the
 // per-node phase dominates there: small CTAs, registers capped at 96 so five
 // fit; measured 20x5: 5.0 G bounds/s vs 3.9 G with one 16-warp CTA); else 16
-template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE, bool BYTE = true>
+// RG (placement ablation, NEXT-3): the couple records are read from global
+// memory (L1/L2, read-only path) instead of the TMA-staged shared buffers.
+template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE, bool BYTE = true, bool RG = false>
 __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM <= 5 ? 5 : 1)
     lb_kernel(const LbArgs a)
 {
@@ -401,11 +404,11 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             mbar_init(s_emp + b, W);
             s_cnt[b] = 0;
         }
-        uint32_t gb = group_blob(0);
+        uint32_t gb = RG ? 0u : group_blob(0);
         mbar_expect_tx(s_bar, gb + (uint32_t)a.L.ptm_bytes);
-        bulk_copy(s_tab, a.tables, gb, s_bar);
+        if (!RG) bulk_copy(s_tab, a.tables, gb, s_bar);
         bulk_copy(smem + a.L.off_ptm, a.ptm, (uint32_t)a.L.ptm_bytes, s_bar);
-        for (int b = 1; dbuf && b < NB && b < nseq; ++b) {
+        for (int b = 1; !RG && dbuf && b < NB && b < nseq; ++b) {
             const int g = b % a.groups;
             gb = group_blob(g);
             mbar_expect_tx(s_bar + b, gb);
@@ -812,7 +815,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             const long long sq = it * a.groups + gi;
             const uint8_t *tab = s_tab;
             mark(PR_WALK);
-            if (dbuf) { // wait for this group's buffer; no CTA-wide barrier
+            if constexpr (RG) {
+                tab = a.tables + (size_t)g * a.L.group_bytes;
+            } else if (dbuf) { // wait for this group's buffer; no CTA-wide barrier
                 const int b = (int)(sq % NB);
                 mbar_wait(s_bar + b, (uint32_t)((sq / NB) & 1), a.wait_ns);
                 tab = s_tab + (size_t)b * a.L.group_bytes;
@@ -992,7 +997,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             }
             } // anyvalid
             mark(PR_WALK);
-            if (dbuf) {
+            if (!RG && dbuf) {
                 // release the buffer; the last of the W warps (its (sq>>1)-th
                 // round of W arrivals completes) refills it with group sq + 2
                 __syncwarp();
@@ -1045,6 +1050,13 @@ __global__ void smem_base_probe(uint32_t *out)
 template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE, bool BYTE = true>
 int launch(const fsp_lb_plan &pl, const LbArgs &a, cudaStream_t s)
 {
+    if constexpr (MAXM == 20 && EXACT && S16 && NPL == 4 && !SPARSE && BYTE) {
+        if (pl.recs_global) {
+            lb_kernel<20, true, true, 4, false, true, true><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
+            cudaError_t e = cudaGetLastError();
+            return e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, "lb_kernel launch");
+        }
+    }
     lb_kernel<MAXM, EXACT, S16, NPL, SPARSE, BYTE><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, "lb_kernel launch");
@@ -1059,6 +1071,11 @@ int configure(fsp_lb_plan &pl)
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          pl.smem_optin);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "cudaFuncSetAttribute");
+    if constexpr (MAXM == 20 && EXACT && S16 && NPL == 4 && !SPARSE && BYTE) {
+        e = cudaFuncSetAttribute(lb_kernel<20, true, true, 4, false, true, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_optin);
+        if (e != cudaSuccess) return fsp_cuda_fail(e, "cudaFuncSetAttribute");
+    }
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM, EXACT, S16, NPL, SPARSE, BYTE>,
                                                       pl.warps * 32, pl.smem_bytes);
@@ -1149,6 +1166,9 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     // sparse walk: exact-m s16 specialisations (records carry the job id),
     // 64 <= n <= 1024 (below 64 jobs the compaction does not pay: measured)
     pl.sparse = sparse && pl.exact && pl.s16 && n >= 64 && n <= 1024;
+    // placement ablation (NEXT-3): couple records read from global memory by
+    // the 20-machine dense byte-row kernel (FSP_LB_RECS=global)
+    pl.recs_global = !sparse && getenv("FSP_LB_RECS") && std::string(getenv("FSP_LB_RECS")) == "global";
     if (pl.exact) pl.maxm = m;
     else if (m <= 8) pl.maxm = 8;
     else if (m <= 16) pl.maxm = 16;

@@ -421,3 +421,19 @@ def test_tune_pool(torch, fsp):
     assert pool in rates and all(r > 0 for r in rates.values())
     assert rates[pool] >= 0.9 * max(rates.values())
     assert all(rates[s] < 0.9 * max(rates.values()) for s in rates if s < pool)
+
+
+@pytest.mark.parametrize("name,N", [("ta021", 20011), ("ta091", 300_000)])
+def test_parity_records_in_global_memory(torch, fsp, orc, monkeypatch, name, N):
+    """Placement ablation (NEXT-3): the walk reading its couple records from
+    global memory (L1/L2) instead of the TMA-staged shared buffers gives the
+    same LBs (sampled against the oracle, all against the default kernel)."""
+    n, m, seed = inputs.TAILLARD_SEEDS[name]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, N, 99)
+    ref = gpu_lb(torch, fsp.Instance(ptm), pf, dp)
+    monkeypatch.setenv("FSP_LB_RECS", "global")
+    got = gpu_lb(torch, fsp.Instance(ptm), pf, dp)
+    assert (got == ref).all()
+    sample = np.random.default_rng(3).choice(N, 500, replace=False)
+    assert (got[sample] == orc.Tables(ptm).lb_eval(pf[sample], dp[sample])).all()
