@@ -194,6 +194,8 @@ struct LbArgs {
                            // its nodes' lb_out entries are zeroed by the host
     unsigned long long *prof; // diagnostics (FSP_LB_PROF): per-phase SM cycles, summed
     uint32_t wait_ns;      // mbarrier try_wait suspend-time hint (0: none)
+    int lane_ingest;       // scheduled-set build with one node per lane (byte and
+                           // lane-major rows); 0: the warp-per-node pass
     int dbg_skip;          // diagnostics only (FSP_LB_DEBUG_SKIP): bit 0 skips the
                            // per-node heads phase, bit 1 the couple walks (LBs wrong)
 };
@@ -500,55 +502,101 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 Uw[j * urow + useg + w] = j < n ? pat[w] : 0u;
         }
         __syncwarp();
-        // coalesced pass over the TN prefix records: clear the scheduled bits
-        // (16-byte rows: each lane takes eight job ids per vector load; the
-        // next node's row is loaded while this one's bits are cleared)
-        const bool rows16 = a.vec_rows && ((reinterpret_cast<uintptr_t>(a.prefix) | ((uintptr_t)a.stride * 2)) & 15) == 0;
+        if (a.lane_ingest && !UL::NIB || a.lane_ingest && UL::BYTES) {
+            // each lane clears the bits of its own nodes: byte rows give lane L
+            // byte L of the row segment (plain byte stores, no other lane
+            // touches it); lane-major rows share a word per 32 nodes (shared
+            // atomics).  All lanes' row loads are in flight at once (one row
+            // per lane, 16-byte vectors) instead of one node at a time.
+            uint8_t *ub = reinterpret_cast<uint8_t *>(Uw + useg) + lane;
+            const int urowB = urow * 4;
 #pragma unroll
-        for (int q = 0; q < NPL; ++q) {
-            if (rows16) {
-                // segment `sg` of node L's row: entries 256*sg .. 256*sg+255
-                auto load_row = [&](int L, int sg) {
-                    const int dL = __shfl_sync(0xffffffffu, dq[q], L);
-                    uint4 v = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-                    if (sg * 256 + lane * 8 < dL)
-                        v = reinterpret_cast<const uint4 *>(a.prefix + (size_t)(tile * TN + q * 32 + L) *
-                                                                           a.stride)[sg * 32 + lane];
-                    return v;
+            for (int q = 0; q < NPL; ++q) {
+                const int d = dq[q];
+                const uint16_t *row = a.prefix + (size_t)(tile * TN + q * 32 + lane) * a.stride;
+                const bool v16 = ((reinterpret_cast<uintptr_t>(a.prefix) | ((uintptr_t)a.stride * 2)) & 15) == 0;
+                auto clear = [&](uint32_t job) {
+                    if (job < (uint32_t)n) {
+                        if constexpr (UL::BYTES) ub[job * urowB] &= (uint8_t)~(2u << q);
+                        else atomicAnd(&Uw[job * urow + useg + q], ~lanebit);
+                    }
                 };
-                // the first segment of the next node is loaded while this
-                // node's bits are cleared
-                uint4 cur = load_row(0, 0);
-                for (int L = 0; L < 32; ++L) {
-                    const int dL = __shfl_sync(0xffffffffu, dq[q], L);
-                    const uint32_t clr = ~(1u << UL::bit(L, q));
-                    const int uwd = useg + UL::word(L, q);
-                    const uint4 nxt = L + 1 < 32 ? load_row(L + 1, 0) : cur;
-                    for (int sg = 0; sg * 256 < dL; ++sg) {
-                        if (sg > 0) cur = load_row(L, sg);
-                        const uint32_t w4[4] = {cur.x, cur.y, cur.z, cur.w};
+                int i = 0;
+                if (v16) {
+                    const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
+                    for (; i + 16 <= d; i += 16) { // two vectors in flight
+                        const uint4 v0 = r4[i >> 3], v1 = r4[(i >> 3) + 1];
+                        const uint32_t w8[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
                         for (int t = 0; t < 8; ++t) {
-                            const uint32_t job = (t & 1) ? (w4[t >> 1] >> 16) : (w4[t >> 1] & 0xffffu);
-                            if (sg * 256 + lane * 8 + t < dL && job < (uint32_t)n)
-                                Uw[job * urow + uwd] &= clr;
+                            clear(w8[t] & 0xffffu);
+                            clear(w8[t] >> 16);
                         }
                     }
-                    __syncwarp();
-                    cur = nxt;
-                }
-            } else {
-                for (int L = 0; L < 32; ++L) {
-                    const int dL = __shfl_sync(0xffffffffu, dq[q], L);
-                    if (dL == 0) continue;
-                    const uint16_t *row = a.prefix + (size_t)(tile * TN + q * 32 + L) * a.stride;
-                    const uint32_t clr = ~(1u << UL::bit(L, q));
-                    const int uwd = useg + UL::word(L, q);
-                    for (int i = lane; i < dL; i += 32) {
-                        const uint32_t job = row[i];
-                        if (job < (uint32_t)n) Uw[job * urow + uwd] &= clr;
+                    if (i < d) {
+                        const uint4 v0 = r4[i >> 3];
+                        const uint4 v1 = i + 8 < d ? r4[(i >> 3) + 1] : v0;
+                        const uint32_t w8[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                        for (int t = 0; t < 16; ++t)
+                            if (i + t < d) clear(t & 1 ? w8[t >> 1] >> 16 : w8[t >> 1] & 0xffffu);
                     }
-                    __syncwarp();
+                } else {
+                    for (; i < d; ++i) clear(row[i]);
+                }
+            }
+            __syncwarp();
+        } else {
+        // coalesced pass over the TN prefix records: clear the scheduled bits
+            // (16-byte rows: each lane takes eight job ids per vector load; the
+            // next node's row is loaded while this one's bits are cleared)
+            const bool rows16 = a.vec_rows && ((reinterpret_cast<uintptr_t>(a.prefix) | ((uintptr_t)a.stride * 2)) & 15) == 0;
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                if (rows16) {
+                    // segment `sg` of node L's row: entries 256*sg .. 256*sg+255
+                    auto load_row = [&](int L, int sg) {
+                        const int dL = __shfl_sync(0xffffffffu, dq[q], L);
+                        uint4 v = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                        if (sg * 256 + lane * 8 < dL)
+                            v = reinterpret_cast<const uint4 *>(a.prefix + (size_t)(tile * TN + q * 32 + L) *
+                                                                               a.stride)[sg * 32 + lane];
+                        return v;
+                    };
+                    // the first segment of the next node is loaded while this
+                    // node's bits are cleared
+                    uint4 cur = load_row(0, 0);
+                    for (int L = 0; L < 32; ++L) {
+                        const int dL = __shfl_sync(0xffffffffu, dq[q], L);
+                        const uint32_t clr = ~(1u << UL::bit(L, q));
+                        const int uwd = useg + UL::word(L, q);
+                        const uint4 nxt = L + 1 < 32 ? load_row(L + 1, 0) : cur;
+                        for (int sg = 0; sg * 256 < dL; ++sg) {
+                            if (sg > 0) cur = load_row(L, sg);
+                            const uint32_t w4[4] = {cur.x, cur.y, cur.z, cur.w};
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) {
+                                const uint32_t job = (t & 1) ? (w4[t >> 1] >> 16) : (w4[t >> 1] & 0xffffu);
+                                if (sg * 256 + lane * 8 + t < dL && job < (uint32_t)n)
+                                    Uw[job * urow + uwd] &= clr;
+                            }
+                        }
+                        __syncwarp();
+                        cur = nxt;
+                    }
+                } else {
+                    for (int L = 0; L < 32; ++L) {
+                        const int dL = __shfl_sync(0xffffffffu, dq[q], L);
+                        if (dL == 0) continue;
+                        const uint16_t *row = a.prefix + (size_t)(tile * TN + q * 32 + L) * a.stride;
+                        const uint32_t clr = ~(1u << UL::bit(L, q));
+                        const int uwd = useg + UL::word(L, q);
+                        for (int i = lane; i < dL; i += 32) {
+                            const uint32_t job = row[i];
+                            if (job < (uint32_t)n) Uw[job * urow + uwd] &= clr;
+                        }
+                        __syncwarp();
+                    }
                 }
             }
         }
@@ -1399,6 +1447,7 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.tail_split = pool_dev ? 1 : fsp_lb_tail_split(pl, pool, a.split);
     a.wait_ns = getenv("FSP_LB_WAIT_NS") ? (uint32_t)atol(getenv("FSP_LB_WAIT_NS")) : 1000000u;
     a.dbg_skip = getenv("FSP_LB_DEBUG_SKIP") ? atoi(getenv("FSP_LB_DEBUG_SKIP")) : 0;
+    a.lane_ingest = getenv("FSP_LB_LANE_INGEST") ? atoi(getenv("FSP_LB_LANE_INGEST")) : 1;
     a.prof = nullptr;
     static unsigned long long *prof_buf = nullptr; // diagnostics only (FSP_LB_PROF=1)
     const bool prof = getenv("FSP_LB_PROF") && atoi(getenv("FSP_LB_PROF")) != 0;
