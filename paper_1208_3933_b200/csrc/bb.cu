@@ -28,6 +28,7 @@
 #include <chrono>
 #include <climits>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -88,6 +89,10 @@ struct BBState {
     BBStatus *d_status, *h_status;
     int64_t last_children; // children of the last iteration (still in ch)
     cudaEvent_t ev_in, ev_out; // ordering against a caller's stream (fsp_bb_step)
+    int order;            // 1: best-first children (R19); 0 (FSP_BB_ORDER=0, A/B): job order, no dive
+    bool timing;          // FSP_BB_TIMING: sum the iterations' device time
+    cudaEvent_t ev_t0, ev_t1;
+    double gpu_ms;
     cudaStream_t stream;
     bool own_stream, sparse;
     fsp_bb_stats stats;
@@ -229,7 +234,7 @@ __global__ void route_kernel(const int32_t *maxnp, const int64_t *count, int fam
 // Rows are 16-byte aligned (stride is a multiple of 8): copies move uint4s.
 __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t *__restrict__ off,
                               Nodes ch, unsigned long long *ch_key, Nodes kp,
-                              const int32_t *__restrict__ ptm, int n, int m, int stride)
+                              const int32_t *__restrict__ ptm, int n, int m, int stride, int by_idle)
 {
     extern __shared__ unsigned long long ex_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -277,7 +282,7 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
                 long long idle = 0;
                 int prev = 0;
                 const int32_t *pj = ptm + (size_t)(cand ? j : 0) * m;
-                for (int k = 0; k < m; ++k) {
+                for (int k = 0; k < (by_idle ? m : 0); ++k) { // (by_idle = 0: job order, A/B only)
                     const int ck = __shfl_sync(0xffffffffu, cpar, k);
                     const int start = max(ck, prev);
                     idle += start - ck;
@@ -406,6 +411,12 @@ __global__ void order_kernel(const int32_t *__restrict__ lb, const unsigned long
         }
         if (lane < g) ord[c0 + r] = (int32_t)(c0 + lane);
     }
+}
+
+__global__ void iota_kernel(int32_t *ord, int64_t cnt)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cnt) ord[i] = (int32_t)i;
 }
 
 // Elimination (a6) + leaves (a8): count survivors per block.
@@ -603,6 +614,11 @@ void bb_free(BBState *s)
     if (s->h_status) cudaFreeHost(s->h_status);
     if (s->ev_in) cudaEventDestroy(s->ev_in);
     if (s->ev_out) cudaEventDestroy(s->ev_out);
+    if (s->ev_t0) cudaEventDestroy(s->ev_t0);
+    if (s->ev_t1) cudaEventDestroy(s->ev_t1);
+    if (s->timing)
+        fprintf(stderr, "FSP_BB_TIMING: %lld iterations, device time %.3f s\n", (long long)s->stats.iterations,
+                s->gpu_ms / 1e3);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
 }
@@ -737,6 +753,7 @@ int bb_iterate(BBState *s)
     // first incumbent (SURVEY.md §8(d) C4 "first dive sets it"); then batches
     const bool dive = s->stats.iterations < s->dive_iters;
     const int K = dive ? 32 : s->K;
+    if (s->timing) cudaEventRecord(s->ev_t0, st);
     // B parents: at most K children each fit the child buffer; the stack grows
     // by at most B*K per iteration and B*K*n over a descent, held under half
     // the capacity (the beam); n*K slots of headroom are always left
@@ -749,8 +766,10 @@ int bb_iterate(BBState *s)
     const int64_t first = s->size - B;
 
     const int pb = 256;
-    cudaError_t e0 = cudaMemsetAsync(s->d_maxnp, 0, 4, st);
-    if (e0 != cudaSuccess) return fsp_cuda_fail(e0, "B&B iteration");
+    if (s->family) {
+        cudaError_t e0 = cudaMemsetAsync(s->d_maxnp, 0, 4, st);
+        if (e0 != cudaSuccess) return fsp_cuda_fail(e0, "B&B iteration");
+    }
     plan_kernel<<<(unsigned)((B + pb - 1) / pb), pb, 0, st>>>(s->st, first, B, n, K, s->d_inc, s->plan,
                                                               s->d_stats, s->d_maxnp);
     device_scan(s, s->plan, nullptr, B, s->off, s->d_count);
@@ -760,7 +779,7 @@ int bb_iterate(BBState *s)
     const int eblocks = (int)std::min<int64_t>((B + ewarps - 1) / ewarps, 148 * 32);
     const size_t esmem = (size_t)ewarps * 8 * (n + ((n + 31) / 32 + 1) / 2);
     expand_kernel<<<eblocks, ewarps * 32, esmem, st>>>(s->st, first, B, s->off, s->ch, s->ch_key,
-                                                       s->kp, inst->d_ptm32, n, m, stride);
+                                                       s->kp, inst->d_ptm32, n, m, stride, s->order);
     const int64_t *off_B = s->off + B; // (kept << 32) | children, on the device
     // bounding (before the kept parents overwrite the popped range): the
     // family kernel from the parents (one of the two launches exits at once),
@@ -778,7 +797,11 @@ int bb_iterate(BBState *s)
         if (rc != FSP_OK) return rc;
     }
     restore_kernel<<<eblocks, ewarps * 32, 0, st>>>(s->kp, off_B, first, s->st, m, stride);
-    order_kernel<<<eblocks, ewarps * 32, 0, st>>>(s->ch.lb, s->ch_key, B, s->off, s->ord);
+    if (s->order) {
+        order_kernel<<<eblocks, ewarps * 32, 0, st>>>(s->ch.lb, s->ch_key, B, s->off, s->ord);
+    } else { // (A/B: children in generation order)
+        iota_kernel<<<(unsigned)((B * K + 255) / 256), 256, 0, st>>>(s->ord, B * K);
+    }
     const int nblk = (int)((maxC + kPruneThreads - 1) / kPruneThreads);
     prune_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->ord, s->d_count, n, s->d_inc, s->d_cand,
                                                   s->bcnt, s->d_stats);
@@ -788,10 +811,16 @@ int bb_iterate(BBState *s)
     commit_kernel<<<1, 256, 0, st>>>(s->ch, n, stride, s->d_inc, s->d_cand, s->d_perm, s->d_packed,
                                      s->rank, off_B, s->boff + nblk, s->d_status);
     cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && s->timing) e = cudaEventRecord(s->ev_t1, st);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(s->h_status, s->d_status, sizeof(BBStatus), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "B&B iteration");
+    if (s->timing) { // diagnostics (FSP_BB_TIMING): device time of the iteration's kernels
+        float ms = 0;
+        cudaEventElapsedTime(&ms, s->ev_t0, s->ev_t1);
+        s->gpu_ms += ms;
+    }
     s->size = first + s->h_status->kept + s->h_status->survivors;
     s->last_children = s->h_status->children;
     s->stats.bounded += s->h_status->children;
@@ -822,7 +851,8 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     s->sparse = getenv("FSP_BB_SPARSE") ? atoi(getenv("FSP_BB_SPARSE")) != 0 : true;
     // children per parent per pop: one lane per child in expand/order, K <= 32
     s->K = (int)std::min<int64_t>(32, std::max<int64_t>(1, env_i64("FSP_BB_K", 8)));
-    s->dive_iters = std::max<int64_t>(0, env_i64("FSP_BB_DIVE", s->n));
+    s->order = env_i64("FSP_BB_ORDER", 1) != 0 ? 1 : 0;
+    s->dive_iters = s->order ? std::max<int64_t>(0, env_i64("FSP_BB_DIVE", s->n)) : 0;
     // sibling-incremental bounding (family.cu) for batches of parents with <= 32
     // unscheduled jobs: measured slower than the sparse walk at the B&B's
     // depth mix, so opt-in (FSP_BB_FAMILY=1)
@@ -876,6 +906,9 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     if (e == cudaSuccess) e = cudaMallocHost((void **)&s->h_status, sizeof(BBStatus));
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming);
+    s->timing = env_i64("FSP_BB_TIMING", 0) != 0;
+    if (e == cudaSuccess && s->timing) e = cudaEventCreate(&s->ev_t0);
+    if (e == cudaSuccess && s->timing) e = cudaEventCreate(&s->ev_t1);
     if (e == cudaSuccess) e = cudaMemcpy(s->d_inc, &s->initial_inc, 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(s->d_cand, 0xff, 8);
     if (e == cudaSuccess) e = cudaMemset(s->d_stats, 0, 16);

@@ -17,6 +17,7 @@ for arg in sys.argv[1:]:
     else:
         rc, ms, perm, st = inst.bb_solve(int(ub), 0, float(secs))
     st["nodes_per_s"] = st["bounded"] / max(st["wall_s"], 1e-9)
+    keep = ("bounded", "iterations", "wall_s", "nodes_per_s")
     print(json.dumps({"instance": name, "threads": threads, "initial_ub": int(ub), "rc": rc,
-                      "makespan": ms, **st}),
+                      "makespan": ms, **{k: st[k] for k in keep}}),
           flush=True)
