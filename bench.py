@@ -45,6 +45,8 @@ def parse():
                          "many nodes (SURVEY.md §8(d) C4: 4M total) instead of 1M each")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-bb", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the other BASELINE configs' bounds/s (bench key other_configs)")
     ap.add_argument("--bb-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--table2", action="store_true",
@@ -468,6 +470,42 @@ def main():
                "h2d_bytes_per_step": int(pf.nbytes + dp.nbytes),
                "d2h_bytes_per_step": int(a.pool * 4)}
 
+    # the other BASELINE.json configs (driver-visible, same run, device-timed):
+    # 20x5, 20x20, 50x20 on 1M-node D1 pools, 500x20 on 262K
+    other = None
+    if not a.no_configs and world == 1 and a.strong_total == 0:
+        other = {}
+        for cfg2, pool2 in (("ta001", 1 << 20), ("ta021", 1 << 20), ("ta051", 1 << 20),
+                            ("ta111", 1 << 18)):
+            if cfg2 == cfg:
+                continue
+            n2, m2, seed2 = inputs.TAILLARD_SEEDS[cfg2]
+            pf2, dp2 = inputs.pool_d1(n2, pool2, inputs.pool_seed(cfg2))
+            i2 = binding.Instance(inputs.taillard(n2, m2, seed2))
+            g_pf = torch.from_numpy(pf2.view(np.int16)).cuda()
+            g_dp = torch.from_numpy(dp2).cuda()
+            g_lb = torch.empty(pool2, dtype=torch.int32, device="cuda")
+            for _ in range(3):
+                i2.lb_eval(g_pf, g_dp, out=g_lb, stream=stream)
+            k2 = 10
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(k2):
+                i2.lb_eval(g_pf, g_dp, out=g_lb, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i2.check() != binding.FSP_OK:
+                raise SystemExit(f"malformed node in the {cfg2} pool")
+            t2 = e0.elapsed_time(e1) / k2 / 1e3
+            ops2 = algorithmic_ops(n2, m2, dp2)
+            other[cfg2] = {"workload": f"{cfg2}-class {n2}x{m2}, D1 pool {pool2}",
+                           "bounds_per_s": pool2 / t2, "ms_per_pool": t2 * 1e3,
+                           "roofline_frac": ops2 / t2 / 1e12 / peak,
+                           "launch": i2.launch_info(pool2)}
+            del g_pf, g_dp, g_lb
+            i2.close()
+
     bb = None
     if not a.no_bb:
         # B&B nodes/sec (BASELINE.json metric, second half): a time-boxed device
@@ -539,7 +577,7 @@ def main():
                          "alu_pipe_peak_tlane_instr_s": alu_pipe_peak,
                          "issue_peak_tlane_instr_s": issue_peak,
                          "ops_per_launch": ops},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": a.steps,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": a.steps, "other_configs": other,
             "clocks": clk.summary(), "bb": bb,
         }
         print(json.dumps(out), flush=True)

@@ -73,7 +73,6 @@ extern "C" int fsp_check(const fsp_instance *inst, void *cuda_stream)
     cudaError_t e = cudaMemcpyAsync(&h, inst->d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "fsp_check");
-    if (h & 2) return fsp_fail(FSP_ECUDA, "lb kernel: dynamic shared-memory base moved");
     if (h) {
         e = cudaMemsetAsync(inst->d_err, 0, sizeof(int), s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);

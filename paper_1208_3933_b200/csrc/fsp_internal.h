@@ -12,7 +12,8 @@
 //   c1   = y = lag_j(k,l) + p_{j,l} = sum_{k<i<=l} p_{j,i}     (int32; s16 walk:
 //          low half, job id j in the high half)
 //   meta = (x << 16) | addr_j   (int32 walk)  or  (addr_j << 16) | (x & 0xffff) (s16 walk)
-//   x = p_{j,l} - p_{j,k} (int16); addr_j = shared-window address of U[j][warp 0]
+//   x = p_{j,l} - p_{j,k} (int16); addr_j = byte offset of U row j (the kernel adds
+//   its own shared-window base)
 // j is the job at this position of the couple's Johnson-with-lags order.
 // DESIGN.md §6 derives the one-update form e <- max(e + x, y) of Fig. 3 lines 11-15.
 // Padding records after the last couple of a group (walk look-ahead).
@@ -52,7 +53,6 @@ struct fsp_lb_plan {
     bool s16;            // 16-bit walk (records in the s16 meta form)
     int npl;             // nodes per lane (2 or 4): U rows are 4*npl bytes per warp
     bool sparse;         // walk only the records of jobs live in the warp (B&B pools)
-    uint32_t smem_base;  // shared-window address of dynamic smem offset 0
     int nrec;            // records per couple (n rounded up to even)
     fsp_lb_layout L;
     int groups;          // couple groups (one resident in smem at a time)

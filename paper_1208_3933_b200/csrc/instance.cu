@@ -34,13 +34,11 @@ static void build_tables(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl
     }
     const size_t gbytes = pl.L.group_bytes;
     const size_t kl_bytes = pl.L.kl_bytes;
-    // shared address of U[j][warp 0] (lane-major rows), or the offset of row j
-    // in a warp's block (nibble rows, s16 with >= 10 machines: the kernel adds
-    // the block base); row n is the always-empty padding row
-    const bool nib = pl.s16 && pl.maxm >= 10; // = ULayout::NIB in lb_kernel.cu
-    auto uaddr = [&](int j) {
-        return (uint32_t)((nib ? 0 : pl.smem_base + pl.L.off_u) + (size_t)j * 4 * pl.L.urow_words);
-    };
+    // byte offset of row j of U (from the U base, lane-major rows; from the
+    // warp's block, byte/nibble rows): the kernel adds the shared-window
+    // address it runs at, so nothing depends on where dynamic shared memory
+    // starts; row n is the always-empty padding row
+    auto uaddr = [&](int j) { return (uint32_t)((size_t)j * 4 * pl.L.urow_words); };
     blob.assign(gbytes * pl.groups, 0);
     for (int g = 0; g < pl.groups; ++g) { // every record slot starts as padding
         fsp_rec *rec = reinterpret_cast<fsp_rec *>(blob.data() + (size_t)g * gbytes + kl_bytes);

@@ -176,7 +176,6 @@ struct LbArgs {
     int *err;
     long long pool;
     const long long *pool_dev; // if set, the pool size is read on the device (B&B)
-    uint32_t smem_base;    // shared-window address the host baked into the records
     fsp_lb_layout L;
     int groups, ppg;       // couple groups, couples per group
     int n, m, P, mp4, nrec;
@@ -203,9 +202,11 @@ struct LbArgs {
 // FSP_LB_PROF phases: cycles lane 0 of every warp spends in each part
 enum { PR_INGEST = 0, PR_HEADS, PR_WAIT, PR_WALK, PR_RELEASE, PR_STORE, PR_N };
 
-// Shared address of U[job][warp] from a record's meta word (wst = 4*NPL*warp).
-//   int32 form: meta = (c2 << 16) | addr    -> (meta & 0xffff) | wst  (one LOP3)
-//   s16 form:   meta = (addr << 16) | c2    -> (meta >> 16) + wst     (one IMAD.HI)
+// Shared address of U[job][warp] from a record's meta word, whose address
+// field is the row's byte offset; wst = the shared-window address of this
+// warp's row segment (the kernel's own, nothing baked in by the host).
+//   int32 form: meta = (c2 << 16) | off     -> (meta & 0xffff) + wst  (one IADD3)
+//   s16 form:   meta = (off << 16) | c2     -> (meta >> 16) + wst     (one IMAD.HI)
 // (hi_mul = 0x10000 arrives as a kernel argument so ptxas keeps an IMAD.HI on
 // the FMA pipe instead of strength-reducing it to an ALU LEA.HI: the ALU pipe
 // is the walk's bottleneck.)
@@ -216,7 +217,7 @@ __device__ __forceinline__ uint32_t mask_addr(uint32_t meta, uint32_t wst, uint3
     // s16: one IMAD.WIDE.U32 with the loop-invariant 64-bit addend wst << 32
     // (a 32-bit "hi + c" form makes ptxas rebuild the {0, c} pair every time)
     if constexpr (S16) return (uint32_t)(((uint64_t)meta * hi_mul + wst64) >> 32);
-    else return (meta & 0xffffu) | wst;
+    else return (meta & 0xffffu) + wst;
 }
 
 // U row layouts (one row per job, one segment per warp):
@@ -350,10 +351,6 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
     // at least one of the warp's nodes (the walk over the others is a no-op)
     uint2 *s_list = reinterpret_cast<uint2 *>(smem + a.L.off_list + (size_t)warp * a.L.list_bytes);
 
-    if (smem_u32(smem) != a.smem_base) { // records carry absolute shared addresses
-        if (threadIdx.x == 0) atomicOr(a.err, 2);
-        return;
-    }
     // TM: the per-node R, A, Q of phase A go to tensor memory, two machines per
     // 32-bit column (16-bit values): column (arr*HM + k/2)*NPL + q of this
     // warp's block in its lane quarter (warp % 4), blocks of TCOLS columns
@@ -443,7 +440,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
     const int lsh = (UL::NIB && !UL::BYTES) ? UL::bit(lane, 0) - 1 : 1;
     const uint32_t shmul = 1u << (32 - lsh);
     const uint32_t wst = UL::BYTES ? smem_u32(Uw) + (uint32_t)lane
-                         : UL::NIB ? smem_u32(Uw) + 4u * lw : 4u * (WPR * warp);
+                         : UL::NIB ? smem_u32(Uw) + 4u * lw : smem_u32(Uw) + 4u * (WPR * warp);
     const int urow = a.L.urow_words; // words per job row of U (padded against bank conflicts)
     const uint32_t hi_mul = a.hi_mul;
     const uint64_t wst64 = (uint64_t)wst << 32;
@@ -502,7 +499,13 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 Uw[j * urow + useg + w] = j < n ? pat[w] : 0u;
         }
         __syncwarp();
-        if (a.lane_ingest && !UL::NIB || a.lane_ingest && UL::BYTES) {
+        // dense pools whose prefix completion times are computed here (no cin):
+        // each lane clears its node's bits in the same pass over the prefix
+        // that computes C (phase A below), reading every prefix once
+        const bool fused = !SPARSE && !a.cin && a.lane_ingest && (!UL::NIB || UL::BYTES);
+        if (fused) {
+            // (scheduled bits cleared in phase A)
+        } else if (a.lane_ingest && !UL::NIB || a.lane_ingest && UL::BYTES) {
             // each lane clears the bits of its own nodes: byte rows give lane L
             // byte L of the row segment (plain byte stores, no other lane
             // touches it); lane-major rows share a word per 32 nodes (shared
@@ -681,23 +684,34 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 }
             };
             const int dd = a.cin ? 0 : d;
+            // fused ingest: also clear this node's bit of each scheduled job's
+            // row (byte rows: lane-owned byte; lane-major: shared atomic)
+            uint8_t *ubq = reinterpret_cast<uint8_t *>(Uw + useg) + lane;
+            auto step_clr = [&](uint32_t job) {
+                if (fused && job < (uint32_t)n) {
+                    if constexpr (UL::BYTES) ubq[job * (urow * 4)] &= (uint8_t)~(2u << q);
+                    else atomicAnd(&Uw[job * urow + useg + q], ~lanebit);
+                }
+                step(job);
+            };
             int i = 0;
             // 16-byte rows: eight job ids per vector load
             if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
                 const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
                 for (; i + 8 <= dd; i += 8) {
                     const uint4 v = r4[i >> 3];
-                    step(v.x & 0xffffu);
-                    step(v.x >> 16);
-                    step(v.y & 0xffffu);
-                    step(v.y >> 16);
-                    step(v.z & 0xffffu);
-                    step(v.z >> 16);
-                    step(v.w & 0xffffu);
-                    step(v.w >> 16);
+                    step_clr(v.x & 0xffffu);
+                    step_clr(v.x >> 16);
+                    step_clr(v.y & 0xffffu);
+                    step_clr(v.y >> 16);
+                    step_clr(v.z & 0xffffu);
+                    step_clr(v.z >> 16);
+                    step_clr(v.w & 0xffffu);
+                    step_clr(v.w >> 16);
                 }
             }
-            for (; i < dd; ++i) step(row[i]);
+            for (; i < dd; ++i) step_clr(row[i]);
+            if (fused) __syncwarp(); // every lane's bits of node group q cleared
             // a2/a3: r_j0 = C_0, r_jk = max(C_k, r_j,k-1 + p_j,k-1) (R3); R_k =
             // min over unscheduled j (R5); Q_l = min_j q_jl, q_jl = sum_{i>l}
             // p_ji (R4); L_k = sum_j p_jk closes the difference walk.
@@ -868,6 +882,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             } else if (dbuf) { // wait for this group's buffer; no CTA-wide barrier
                 const int b = (int)(sq % NB);
                 mbar_wait(s_bar + b, (uint32_t)((sq / NB) & 1), a.wait_ns);
+                __syncwarp(); // reconverged before the .sync.aligned TMEM loads
                 tab = s_tab + (size_t)b * a.L.group_bytes;
             } else if (g != resident) {
                 __syncthreads(); // every warp is done with the resident group
@@ -1066,6 +1081,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                                   a.tables + (size_t)gn * a.L.group_bytes, gb, s_bar + b);
                     }
                 }
+                __syncwarp(); // lane 0 may have waited on "released": reconverge
             }
             mark(PR_RELEASE);
         }
@@ -1087,12 +1103,6 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (warp == 0) tm_dealloc(*s_tm, a.tm_cols);
     }
-}
-
-__global__ void smem_base_probe(uint32_t *out)
-{
-    extern __shared__ __align__(128) uint8_t smem[];
-    *out = smem_u32(smem);
 }
 
 template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE, bool BYTE = true>
@@ -1175,21 +1185,6 @@ static int occupancy_of(fsp_lb_plan &pl)
     return FSP_OK;
 }
 
-static int probe_smem_base(uint32_t *base)
-{
-    uint32_t *d = nullptr, h = 0;
-    cudaError_t e = cudaMalloc(&d, sizeof(uint32_t));
-    if (e == cudaSuccess) {
-        smem_base_probe<<<1, 1, 16>>>(d);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = cudaMemcpy(&h, d, sizeof(uint32_t), cudaMemcpyDeviceToHost);
-    cudaFree(d);
-    if (e != cudaSuccess) return fsp_cuda_fail(e, "smem base probe");
-    *base = h;
-    return FSP_OK;
-}
-
 // couple-group buffers per CTA when the couples take several groups
 // (FSP_LB_DBUF: 0/1 = one buffer + CTA barrier, 2..FSP_MAX_GBUF = multi-buffered)
 static int nbuf_want()
@@ -1228,8 +1223,6 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     if (e != cudaSuccess) return fsp_cuda_fail(e, "device attribute");
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "device attribute");
-    int rc = probe_smem_base(&pl.smem_base);
-    if (rc != FSP_OK) return rc;
     pl.num_sms = sms;
     pl.smem_optin = optin;
     const int mp4 = (m + 3) & ~3;
@@ -1260,9 +1253,6 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
             // of 4 leaves some SMSPs with an extra warp that paces the whole CTA
             // (measured: 200x20, 10 warps 120 M/s vs 12 warps 140 M/s)
             if (W % 4 != 0 && w_lo != w_hi) continue;
-            // int32 walk ORs the warp offset into the record address: 4*npl*W
-            // must be a power of two (s16 adds it on the FMA pipe instead)
-            if (!pl.s16 && ((4 * npl * W) & (4 * npl * W - 1))) continue;
             // sparse-plan rows are padded by npl words so the per-job rows of
             // one warp spread over the banks (building U touches 32 different
             // jobs at once; it dominates for deep B&B nodes, not for D1 pools)
@@ -1275,7 +1265,7 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
             // nibble: per-warp blocks of (n+1) rows of wpr|1 words (odd: the 32 jobs a
             // warp clears at once hit 32 banks); record offsets j*4*urow < 64 KB
             const int urow = nib ? wpr | 1 : npl * W;
-            if (!nib && pl.smem_base + (size_t)(n + 1) * 4 * urow > 65536) continue; // 16-bit U addresses
+            if (!nib && (size_t)(n + 1) * 4 * urow > 65535) continue; // 16-bit U row offsets
             if (nib && (size_t)(n + 1) * 4 * urow > 65535) continue;
             fsp_lb_layout L{};
             L.urow_words = urow;
@@ -1429,7 +1419,6 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.err = inst->d_err;
     a.pool = pool;
     a.pool_dev = reinterpret_cast<const long long *>(pool_dev);
-    a.smem_base = pl.smem_base;
     a.L = pl.L;
     a.groups = pl.groups;
     a.ppg = pl.pairs_per_group;
