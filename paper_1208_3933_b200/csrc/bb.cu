@@ -239,9 +239,10 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
     extern __shared__ unsigned long long ex_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int nw = (n + 31) >> 5;
-    // per warp: keys[n] u64 | bm[nw] u32
-    unsigned long long *keys = ex_smem + (size_t)wib * (n + (nw + 1) / 2);
+    // per warp: keys[n] u64 | bm[nw] u32 | parent C[m] int32 (cs)
+    unsigned long long *keys = ex_smem + (size_t)wib * (n + (nw + 1) / 2 + 16);
     uint32_t *bm = reinterpret_cast<uint32_t *>(keys + n);
+    int32_t *cs = reinterpret_cast<int32_t *>(keys + n + (nw + 1) / 2);
     const int s8 = stride >> 3; // uint4 per row
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; p < B; p += warps) {
@@ -268,30 +269,33 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
                 }
             }
             __syncwarp();
-            // candidates: the unscheduled jobs, each keyed (idle << 12) | j by the
-            // idle time appending it opens on the machines (R19): machine k,
-            // free at C_k, waits until j leaves machine k-1.  Compacted in j
-            // order into keys[0..nc).
-            const int32_t cpar = lane < m ? st.C[(size_t)src * m + lane] : 0;
+            // candidates: the unscheduled jobs, compacted in j order into
+            // keys[0..nc), then keyed (idle << 12) | j, lane per candidate, by
+            // the idle time appending each opens on the machines (R19):
+            // machine k, free at C_k, waits until j leaves machine k-1
+            for (int k = lane; k < m; k += 32) cs[k] = st.C[(size_t)src * m + k];
             int nc = 0;
             for (int w = 0; w < nw; ++w) {
                 const int j = w * 32 + lane;
                 const bool cand = j < n && !(bm[w] >> lane & 1);
                 const unsigned bal = __ballot_sync(0xffffffffu, cand);
-                if (!bal) continue;
+                if (cand) keys[nc + __popc(bal & ((1u << lane) - 1))] = (unsigned long long)j;
+                nc += __popc(bal);
+            }
+            __syncwarp();
+            for (int i = lane; i < nc; i += 32) {
+                const int j = (int)keys[i];
                 long long idle = 0;
                 int prev = 0;
-                const int32_t *pj = ptm + (size_t)(cand ? j : 0) * m;
+                const int32_t *pj = ptm + (size_t)j * m;
+#pragma unroll 4
                 for (int k = 0; k < (by_idle ? m : 0); ++k) { // (by_idle = 0: job order, A/B only)
-                    const int ck = __shfl_sync(0xffffffffu, cpar, k);
+                    const int ck = cs[k];
                     const int start = max(ck, prev);
                     idle += start - ck;
-                    prev = start + pj[k];
+                    prev = start + __ldg(pj + k);
                 }
-                if (cand)
-                    keys[nc + __popc(bal & ((1u << lane) - 1))] =
-                        ((unsigned long long)idle << 12) | (unsigned)j;
-                nc += __popc(bal);
+                keys[i] = ((unsigned long long)idle << 12) | (unsigned)j;
             }
             __syncwarp();
             // children of this pop: the g smallest keys above the last key taken
@@ -777,7 +781,7 @@ int bb_iterate(BBState *s)
         route_kernel<<<1, 1, 0, st>>>(s->d_maxnp, s->d_count, 1, s->d_famflag, s->d_count_sparse);
     const int ewarps = n > 1024 ? 1 : 4;
     const int eblocks = (int)std::min<int64_t>((B + ewarps - 1) / ewarps, 148 * 32);
-    const size_t esmem = (size_t)ewarps * 8 * (n + ((n + 31) / 32 + 1) / 2);
+    const size_t esmem = (size_t)ewarps * 8 * (n + ((n + 31) / 32 + 1) / 2 + 16);
     expand_kernel<<<eblocks, ewarps * 32, esmem, st>>>(s->st, first, B, s->off, s->ch, s->ch_key,
                                                        s->kp, inst->d_ptm32, n, m, stride, s->order);
     const int64_t *off_B = s->off + B; // (kept << 32) | children, on the device

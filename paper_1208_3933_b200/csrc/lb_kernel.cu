@@ -655,9 +655,23 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             const uint16_t *row = a.prefix + (size_t)(d ? node : 0) * a.stride;
             if (a.cin) { // completion times supplied (B&B children: parent C + one job)
                 if (node < pool) {
+                    const int32_t *cr = a.cin + (size_t)node * a.cin_stride;
+                    if ((reinterpret_cast<uintptr_t>(cr) & 15) == 0) { // 16-byte rows: vectors
 #pragma unroll
-                    for (int k = 0; k < MAXM; ++k)
-                        if (k < m) C[k] = a.cin[(size_t)node * a.cin_stride + k];
+                        for (int k4 = 0; k4 < (MAXM + 3) / 4; ++k4) {
+                            if (4 * k4 < m) {
+                                const int4 v = reinterpret_cast<const int4 *>(cr)[k4];
+                                const int cv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                                for (int t = 0; t < 4; ++t)
+                                    if (4 * k4 + t < MAXM && 4 * k4 + t < m) C[4 * k4 + t] = cv[t];
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < MAXM; ++k)
+                            if (k < m) C[k] = cr[k];
+                    }
                 }
             }
             auto step = [&](uint32_t job) {
