@@ -62,12 +62,14 @@ struct BBState {
     const fsp_instance *inst;
     int rank, world, n, m, stride, K;
     int64_t dive_iters;   // iterations of the first single-parent dive
+    double beam;          // a descent of n levels may fill this fraction of the stack
     int64_t cap;          // stack capacity (nodes)
     int64_t base, size;   // open nodes live in [base, size)
     int64_t ccap;         // children per iteration (buffer capacity)
     int64_t kcap;         // parents per iteration
     Nodes st, kp, ch;     // stack, kept parents (scratch), children
     unsigned long long *ch_key; // per child: (idle << 12) | j (R19 tie key)
+    uint16_t *ch_uf;      // per child: its unscheduled jobs (n - depth entries, stride)
     int32_t *ord;         // child slot -> child record, siblings by descending (LB, key)
     int32_t *d_maxnp;     // largest |S| among this iteration's expanded parents
     int32_t *d_famflag;   // 1: the family kernel bounds this iteration's children
@@ -233,7 +235,7 @@ __global__ void route_kernel(const int32_t *maxnp, const int64_t *count, int fam
 // A parent with children left is copied to the kept buffer, cursor advanced.
 // Rows are 16-byte aligned (stride is a multiple of 8): copies move uint4s.
 __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t *__restrict__ off,
-                              Nodes ch, unsigned long long *ch_key, Nodes kp,
+                              Nodes ch, unsigned long long *ch_key, uint16_t *ch_uf, Nodes kp,
                               const int32_t *__restrict__ ptm, int n, int m, int stride, int by_idle)
 {
     extern __shared__ unsigned long long ex_smem[];
@@ -318,6 +320,25 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
             }
             klast = thr;
             const int myj = lane < g ? (int)(mykey & 0xfffu) : -1;
+            // each child's unscheduled jobs (the bounding kernel's input: n' - 1
+            // entries instead of a d + 1 prefix): the parent's candidates, in
+            // job order, without the child's own job
+            if (ch_uf) {
+                const unsigned lt = (1u << lane) - 1u;
+                for (int t = 0; t < g; ++t) {
+                    const int xj = __shfl_sync(0xffffffffu, myj, t);
+                    uint16_t *ur = ch_uf + (size_t)(c0 + t) * stride;
+                    int base = 0;
+                    for (int i0 = 0; i0 < nc; i0 += 32) {
+                        const int i = i0 + lane;
+                        const int j = i < nc ? (int)(keys[i] & 0xfffu) : -1;
+                        const bool keep = i < nc && j != xj;
+                        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                        if (keep) ur[base + __popc(bal & lt)] = (uint16_t)j;
+                        base += __popc(bal);
+                    }
+                }
+            }
             __syncwarp(); // keys are rewritten by the warp's next parent
             // prefixes: every child row = the parent's row with its job at d
             for (int t = 0; t < g; ++t) {
@@ -597,6 +618,7 @@ void bb_free(BBState *s)
     free_nodes(s->kp);
     free_nodes(s->ch);
     cudaFree(s->ch_key);
+    cudaFree(s->ch_uf);
     cudaFree(s->ord);
     cudaFree(s->d_maxnp);
     cudaFree(s->d_famflag);
@@ -763,7 +785,7 @@ int bb_iterate(BBState *s)
     // the capacity (the beam); n*K slots of headroom are always left
     const int64_t usable = s->cap - (int64_t)n * K;
     int64_t B = std::min<int64_t>(open, std::min<int64_t>(s->kcap, s->ccap / K));
-    B = std::min<int64_t>(B, std::max<int64_t>(1, s->cap / 2 / ((int64_t)K * n)));
+    B = std::min<int64_t>(B, std::max<int64_t>(1, (int64_t)(s->cap * s->beam) / ((int64_t)K * n)));
     B = std::min<int64_t>(B, std::max<int64_t>(1, (usable - s->size) / K));
     if (dive) B = 1;
     if (s->size + B * K > s->cap) return fsp_fail(FSP_ENOMEM, "B&B stack full");
@@ -783,7 +805,8 @@ int bb_iterate(BBState *s)
     const int eblocks = (int)std::min<int64_t>((B + ewarps - 1) / ewarps, 148 * 32);
     const size_t esmem = (size_t)ewarps * 8 * (n + ((n + 31) / 32 + 1) / 2 + 16);
     expand_kernel<<<eblocks, ewarps * 32, esmem, st>>>(s->st, first, B, s->off, s->ch, s->ch_key,
-                                                       s->kp, inst->d_ptm32, n, m, stride, s->order);
+                                                       s->ch_uf, s->kp, inst->d_ptm32, n, m, stride,
+                                                       s->order);
     const int64_t *off_B = s->off + B; // (kept << 32) | children, on the device
     // bounding (before the kept parents overwrite the popped range): the
     // family kernel from the parents (one of the two launches exits at once),
@@ -792,7 +815,7 @@ int bb_iterate(BBState *s)
     const int64_t maxC = B * K;
     int rc = fsp_launch_lb_dev(inst, s->ch.pf, stride, s->ch.dp, maxC,
                                s->family ? s->d_count_sparse : s->d_count, s->ch.C, m, s->sparse, s->ch.lb,
-                               st);
+                               st, 0, s->ch_uf);
     if (rc != FSP_OK) return rc;
     if (s->family) {
         rc = fsp_launch_family(inst, s->st.pf + (size_t)first * stride, stride, s->st.dp + first,
@@ -856,6 +879,12 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     // children per parent per pop: one lane per child in expand/order, K <= 32
     s->K = (int)std::min<int64_t>(32, std::max<int64_t>(1, env_i64("FSP_BB_K", 8)));
     s->order = env_i64("FSP_BB_ORDER", 1) != 0 ? 1 : 0;
+    // the beam: B*K*n <= beam * capacity.  A descent pushes at most B*K nodes
+    // per level, and every iteration's B is also held to the free stack
+    // (usable - size) / K, so a beam above 1 never overflows: near a full stack
+    // the batches shrink.  Measured at 200x20 (profiles/r02/bb_beam.txt):
+    // 0.5 -> 4.7e8 nodes/s, 2 -> 5.9e8, 4 -> 6.3e8 (30 s), 8 no further gain
+    s->beam = getenv("FSP_BB_BEAM") ? atof(getenv("FSP_BB_BEAM")) : 4.0;
     s->dive_iters = s->order ? std::max<int64_t>(0, env_i64("FSP_BB_DIVE", s->n)) : 0;
     // sibling-incremental bounding (family.cu) for batches of parents with <= 32
     // unscheduled jobs: measured slower than the sparse walk at the B&B's
@@ -872,7 +901,7 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     size_t freeb = 0, totalb = 0;
     if (e == cudaSuccess) e = cudaMemGetInfo(&freeb, &totalb);
     // children per iteration: enough to fill the GPU several times over
-    s->ccap = std::max<int64_t>(children_cap > 0 ? children_cap : env_i64("FSP_BB_CHILDREN", 1 << 21), 32);
+    s->ccap = std::max<int64_t>(children_cap > 0 ? children_cap : env_i64("FSP_BB_CHILDREN", 1 << 22), 32);
     s->kcap = s->ccap;
     // the stack takes most of the free HBM (180 GB per B200)
     const double frac = mem_frac > 0 ? mem_frac
@@ -889,6 +918,10 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
         if (e == cudaSuccess) e = cudaMalloc(p, bytes);
     };
     alloc((void **)&s->ch_key, (size_t)s->ccap * 8);
+    // unscheduled lists for the sparse byte-row bounding plan (long prefixes:
+    // deep children have n' << d); measured slower for n < 64 (dense plan)
+    if (env_i64("FSP_BB_ULIST", 1) != 0 && inst->plan_bb.sparse && inst->plan_bb.byte_rows)
+        alloc((void **)&s->ch_uf, (size_t)s->ccap * s->stride * 2);
     alloc((void **)&s->ord, (size_t)s->ccap * 4);
     alloc((void **)&s->d_maxnp, 4);
     alloc((void **)&s->d_famflag, 4);

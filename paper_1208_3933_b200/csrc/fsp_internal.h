@@ -125,7 +125,9 @@ int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stri
 // sparse-walk plan (B&B child pools)
 // grid_limit > 0: at most that many CTAs (the host path leaves SMs to its
 // PCIe gather kernel)
+// ulist != nullptr (with cin, byte-row plans): each node's unscheduled jobs,
+// n - depth entries per row; the prefix rows are then not read
 int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                       const int32_t *depth, int64_t pool, const int64_t *pool_dev,
                       const int32_t *cin, int32_t cin_stride, bool sparse, int32_t *lb_out,
-                      cudaStream_t s, int grid_limit = 0);
+                      cudaStream_t s, int grid_limit = 0, const uint16_t *ulist = nullptr);

@@ -193,6 +193,10 @@ struct LbArgs {
                            // its nodes' lb_out entries are zeroed by the host
     unsigned long long *prof; // diagnostics (FSP_LB_PROF): per-phase SM cycles, summed
     uint32_t wait_ns;      // mbarrier try_wait suspend-time hint (0: none)
+    const uint16_t *ulist; // B&B pools (nullable): node i's unscheduled jobs, n - depth[i]
+                           // entries of row i (same stride); the prefix is then not read
+                           // (completion times come from cin): rows start empty and each
+                           // lane SETS its node's bits (deep nodes: n' << d entries)
     int lane_ingest;       // scheduled-set build with one node per lane (byte and
                            // lane-major rows); 0: the warp-per-node pass
     int dbg_skip;          // diagnostics only (FSP_LB_DEBUG_SKIP): bit 0 skips the
@@ -496,7 +500,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
         for (int j = lane; j <= n; j += 32) {
 #pragma unroll
             for (int w = 0; w < WPR; ++w) // row n: the padding record's always-empty mask
-                Uw[j * urow + useg + w] = j < n ? pat[w] : 0u;
+                Uw[j * urow + useg + w] = j < n && !a.ulist ? pat[w] : 0u;
         }
         __syncwarp();
         // dense pools whose prefix completion times are computed here (no cin):
@@ -513,15 +517,22 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             // per lane, 16-byte vectors) instead of one node at a time.
             uint8_t *ub = reinterpret_cast<uint8_t *>(Uw + useg) + lane;
             const int urowB = urow * 4;
+            const bool setm = UL::BYTES && a.ulist != nullptr; // set unscheduled bits instead
+            const uint16_t *src = setm ? a.ulist : a.prefix;
 #pragma unroll
             for (int q = 0; q < NPL; ++q) {
-                const int d = dq[q];
-                const uint16_t *row = a.prefix + (size_t)(tile * TN + q * 32 + lane) * a.stride;
-                const bool v16 = ((reinterpret_cast<uintptr_t>(a.prefix) | ((uintptr_t)a.stride * 2)) & 15) == 0;
+                const long long node = tile * TN + q * 32 + lane;
+                const int d = setm ? (node < pool ? n - dq[q] : 0) : dq[q];
+                const uint16_t *row = src + (size_t)node * a.stride;
+                const bool v16 = ((reinterpret_cast<uintptr_t>(src) | ((uintptr_t)a.stride * 2)) & 15) == 0;
                 auto clear = [&](uint32_t job) {
                     if (job < (uint32_t)n) {
-                        if constexpr (UL::BYTES) ub[job * urowB] &= (uint8_t)~(2u << q);
-                        else atomicAnd(&Uw[job * urow + useg + q], ~lanebit);
+                        if constexpr (UL::BYTES) {
+                            if (setm) ub[job * urowB] |= (uint8_t)(2u << q);
+                            else ub[job * urowB] &= (uint8_t)~(2u << q);
+                        } else {
+                            atomicAnd(&Uw[job * urow + useg + q], ~lanebit);
+                        }
                     }
                 };
                 int i = 0;
@@ -1122,9 +1133,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
 template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE, bool BYTE = true>
 int launch(const fsp_lb_plan &pl, const LbArgs &a, cudaStream_t s)
 {
-    if constexpr (MAXM == 20 && EXACT && S16 && NPL == 4 && !SPARSE && BYTE) {
+    if constexpr (MAXM == 20 && EXACT && S16 && NPL == 4 && BYTE) {
         if (pl.recs_global) {
-            lb_kernel<20, true, true, 4, false, true, true><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
+            lb_kernel<20, true, true, 4, SPARSE, true, true><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
             cudaError_t e = cudaGetLastError();
             return e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, "lb_kernel launch");
         }
@@ -1143,8 +1154,8 @@ int configure(fsp_lb_plan &pl)
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          pl.smem_optin);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "cudaFuncSetAttribute");
-    if constexpr (MAXM == 20 && EXACT && S16 && NPL == 4 && !SPARSE && BYTE) {
-        e = cudaFuncSetAttribute(lb_kernel<20, true, true, 4, false, true, true>,
+    if constexpr (MAXM == 20 && EXACT && S16 && NPL == 4 && BYTE) {
+        e = cudaFuncSetAttribute(lb_kernel<20, true, true, 4, SPARSE, true, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_optin);
         if (e != cudaSuccess) return fsp_cuda_fail(e, "cudaFuncSetAttribute");
     }
@@ -1225,7 +1236,10 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     pl.sparse = sparse && pl.exact && pl.s16 && n >= 64 && n <= 1024;
     // placement ablation (NEXT-3): couple records read from global memory by
     // the 20-machine dense byte-row kernel (FSP_LB_RECS=global)
-    pl.recs_global = !sparse && getenv("FSP_LB_RECS") && std::string(getenv("FSP_LB_RECS")) == "global";
+    {
+        const char *rg = getenv(sparse ? "FSP_BB_RECS" : "FSP_LB_RECS");
+        pl.recs_global = rg && std::string(rg) == "global";
+    }
     if (pl.exact) pl.maxm = m;
     else if (m <= 8) pl.maxm = 8;
     else if (m <= 16) pl.maxm = 16;
@@ -1413,7 +1427,7 @@ int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stri
 int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                       const int32_t *depth, int64_t pool, const int64_t *pool_dev,
                       const int32_t *cin, int32_t cin_stride, bool sparse, int32_t *lb_out,
-                      cudaStream_t s, int grid_limit)
+                      cudaStream_t s, int grid_limit, const uint16_t *ulist)
 {
     fsp_lb_plan pl = sparse ? inst->plan_bb : inst->plan;
     // host path: a few SMs are left to the PCIe gather kernel of the next chunk
@@ -1451,6 +1465,8 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.wait_ns = getenv("FSP_LB_WAIT_NS") ? (uint32_t)atol(getenv("FSP_LB_WAIT_NS")) : 1000000u;
     a.dbg_skip = getenv("FSP_LB_DEBUG_SKIP") ? atoi(getenv("FSP_LB_DEBUG_SKIP")) : 0;
     a.lane_ingest = getenv("FSP_LB_LANE_INGEST") ? atoi(getenv("FSP_LB_LANE_INGEST")) : 1;
+    // unscheduled lists: byte-row plans with supplied completion times only
+    a.ulist = ulist && cin && pl.s16 && pl.maxm >= 10 && pl.byte_rows && a.lane_ingest ? ulist : nullptr;
     a.prof = nullptr;
     static unsigned long long *prof_buf = nullptr; // diagnostics only (FSP_LB_PROF=1)
     const bool prof = getenv("FSP_LB_PROF") && atoi(getenv("FSP_LB_PROF")) != 0;
