@@ -514,9 +514,37 @@ def main():
         try:
             from paper_1208_3933_b200 import dist as fdist
             if world == 1:
-                rc, msp, perm, st = inst.bb_solve(2**31 - 1, 0, a.bb_seconds)
-                bb = {"bounded_nodes_per_s": st["bounded"] / max(st["wall_s"], 1e-9),
-                      "status": int(rc), "incumbent": msp, **st}
+                # the step API in a host loop so the incumbent trajectory (SURVEY.md
+                # §8(d) C4) is recorded; each step is one device iteration
+                state = binding.BBState(inst)
+                traj = []
+                t_start = time.perf_counter()
+                best = 2**31 - 1
+                while state.pool_size() > 0:
+                    state.step(1)
+                    el = time.perf_counter() - t_start
+                    inc = state.ub_get() >> 32
+                    if inc < best:
+                        best = inc
+                        traj.append([round(el, 4), int(inc), int(state.stats()["bounded"])])
+                    if el >= a.bb_seconds:
+                        break
+                wall = time.perf_counter() - t_start
+                st = state.stats()
+                done = state.pool_size() == 0
+                rcb, msp, permb = state.result()
+                if rcb == 0 and schedule_makespan(ptm, permb) != msp:
+                    raise SystemExit("B&B incumbent does not match its schedule")
+                bb = {"bounded_nodes_per_s": st["bounded"] / max(wall, 1e-9),
+                      # per-node roofline of the B&B: Fig. 3 operations of every
+                      # bounded child (fsp_lb_work at its depth) per second of the
+                      # whole search (branching, compaction included) / the peak
+                      "roofline_frac_of_search": st["lb_ops"] / max(wall, 1e-9) / 1e12 / peak,
+                      "status": 0 if done and rcb == 0 else (-6 if rcb == 0 else int(rcb)),
+                      "incumbent": msp, "incumbent_verified": rcb == 0,
+                      "ub_trajectory_s_ub_bounded": traj,
+                      **{k: v for k, v in st.items() if k != "wall_s"}, "wall_s": wall}
+                state.close()
             else:
                 state = binding.BBState(inst, 2**31 - 1, rank, world)
                 eng = fdist.DeviceEngine(state, "cuda", comm)

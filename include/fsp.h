@@ -213,6 +213,7 @@ typedef struct {
     int64_t leaves;       /* complete schedules evaluated                  */
     int64_t iterations;   /* device expand/bound/prune steps               */
     double wall_s;        /* host wall time of the solve                   */
+    int64_t lb_ops;       /* sum of fsp_lb_work over the bounded children  */
 } fsp_bb_stats;
 
 int fsp_bb_solve(const fsp_instance *inst, int32_t initial_ub, int64_t max_nodes,

@@ -56,7 +56,8 @@ class LaunchInfo(C.Structure):
 
 class BBStats(C.Structure):
     _fields_ = [("bounded", C.c_int64), ("branched", C.c_int64), ("pruned", C.c_int64),
-                ("leaves", C.c_int64), ("iterations", C.c_int64), ("wall_s", C.c_double)]
+                ("leaves", C.c_int64), ("iterations", C.c_int64), ("wall_s", C.c_double),
+                ("lb_ops", C.c_int64)]
 
 
 _lib = None

@@ -446,7 +446,7 @@ __global__ void iota_kernel(int32_t *ord, int64_t cnt)
 
 // Elimination (a6) + leaves (a8): count survivors per block.
 __global__ void __launch_bounds__(kPruneThreads)
-    prune_kernel(Nodes ch, const int32_t *__restrict__ ord, const int64_t *count, int n,
+    prune_kernel(Nodes ch, const int32_t *__restrict__ ord, const int64_t *count, int n, int m,
                  const int32_t *inc_dev, unsigned long long *cand, int32_t *bcnt,
                  unsigned long long *stats)
 {
@@ -460,9 +460,12 @@ __global__ void __launch_bounds__(kPruneThreads)
     const int inc = *inc_dev;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int survive = 0, pruned = 0, leaf = 0;
+    unsigned long long w = 0; // Fig. 3 / Table I operations of this child's bound (§7)
     if (i < C) {
         const int32_t rec = ord[i];
         const int d = ch.dp[rec], lb = ch.lb[rec];
+        const unsigned long long P = (unsigned long long)m * (m - 1) / 2, np = (unsigned)(n - d);
+        w = 2ull * d * m + np * (3ull * m - 2) + np * m + P * n + 4ull * P * np + 2ull * P;
         if (d >= n - 1) { // complete or forced completion: LB is its makespan (R6, P4)
             leaf = 1;
             if (lb < inc) atomicMin(cand, ((unsigned long long)(unsigned)lb << 32) | (unsigned)rec);
@@ -475,6 +478,8 @@ __global__ void __launch_bounds__(kPruneThreads)
     const int cs = __syncthreads_count(survive);
     const int cp = __syncthreads_count(pruned);
     const int cl = __syncthreads_count(leaf);
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(&stats[2], w);
     if (threadIdx.x == 0) {
         bcnt[blockIdx.x] = cs;
         if (cp) atomicAdd(&stats[0], (unsigned long long)cp);
@@ -830,7 +835,7 @@ int bb_iterate(BBState *s)
         iota_kernel<<<(unsigned)((B * K + 255) / 256), 256, 0, st>>>(s->ord, B * K);
     }
     const int nblk = (int)((maxC + kPruneThreads - 1) / kPruneThreads);
-    prune_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->ord, s->d_count, n, s->d_inc, s->d_cand,
+    prune_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->ord, s->d_count, n, m, s->d_inc, s->d_cand,
                                                   s->bcnt, s->d_stats);
     device_scan(s, nullptr, s->bcnt, nblk, s->boff, nullptr);
     scatter_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->ord, s->d_count, off_B, n, m, stride,
@@ -938,7 +943,7 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     alloc((void **)&s->d_packed, 8);
     alloc((void **)&s->d_scratch, 8);
     alloc((void **)&s->d_perm, (size_t)n * 4);
-    alloc((void **)&s->d_stats, 16);
+    alloc((void **)&s->d_stats, 24);
     alloc((void **)&s->d_status, sizeof(BBStatus));
     if (e == cudaSuccess) e = cudaMallocHost((void **)&s->h_status, sizeof(BBStatus));
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming);
@@ -948,7 +953,7 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     if (e == cudaSuccess && s->timing) e = cudaEventCreate(&s->ev_t1);
     if (e == cudaSuccess) e = cudaMemcpy(s->d_inc, &s->initial_inc, 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(s->d_cand, 0xff, 8);
-    if (e == cudaSuccess) e = cudaMemset(s->d_stats, 0, 16);
+    if (e == cudaSuccess) e = cudaMemset(s->d_stats, 0, 24);
     if (e == cudaSuccess) {
         const long long pk = ((long long)INT32_MAX << 32) | (unsigned)rank; // no schedule yet
         e = cudaMemcpy(s->d_packed, &pk, 8, cudaMemcpyHostToDevice);
@@ -989,12 +994,13 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
 
 int read_stats(BBState *s)
 {
-    unsigned long long h[2] = {0, 0};
-    cudaError_t e = cudaMemcpyAsync(h, s->d_stats, 16, cudaMemcpyDeviceToHost, s->stream);
+    unsigned long long h[3] = {0, 0, 0};
+    cudaError_t e = cudaMemcpyAsync(h, s->d_stats, 24, cudaMemcpyDeviceToHost, s->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "B&B stats");
     s->stats.pruned = (int64_t)h[0];
     s->stats.leaves = (int64_t)h[1];
+    s->stats.lb_ops = (int64_t)h[2];
     return FSP_OK;
 }
 

@@ -194,6 +194,7 @@ extern "C" int fsp_bb_solve_hybrid(const fsp_instance *inst, int32_t initial_ub,
         tot.pruned += s1.pruned;
         tot.leaves += s1.leaves;
         tot.iterations += s1.iterations;
+        tot.lb_ops += s1.lb_ops;
         int32_t ms = -1;
         std::vector<int32_t> p(inst->n);
         const int r1 = fsp_bb_result(st[t], &ms, p.data());

@@ -42,4 +42,25 @@ run("ta111", 129)
 rng = np.random.default_rng(1)
 p = rng.integers(1, 50, (8, 4)).astype(np.int32)
 print(binding.Instance(p).bb_solve()[:2], flush=True)
+# round 2: B&B with ordering / dive / unscheduled lists (ta091 few iterations),
+# the family kernel, the hybrid solver, the pinned-host gather path
+os.environ["FSP_BB_CHILDREN"] = "8192"
+os.environ["FSP_BB_MEM_FRAC"] = "0.02"
+inst = binding.Instance(inputs.instance("ta091"))
+bb = binding.BBState(inst)
+bb.step(12)
+print("bb ta091", bb.stats()["bounded"], flush=True)
+bb.close()
+i20 = binding.Instance(inputs.instance("ta021"))
+pf, dp = inputs.pool_fixed_depth(20, 64, 8, 3)
+print("family", int(i20.lb_eval_children(torch.from_numpy(pf.view(np.int16)).cuda(),
+                                        torch.from_numpy(dp).cuda()).sum().item()), flush=True)
+print("hybrid", binding.Instance(p).bb_solve_hybrid(2)[:2], flush=True)
+n = 200
+pf, dp = inputs.pool_d1(n, 148 * 16 * 128 + 77, 9)
+h_pf = torch.from_numpy(pf.view(np.int16)).pin_memory()
+h_dp = torch.from_numpy(dp).pin_memory()
+h_lb = torch.empty(len(dp), dtype=torch.int32).pin_memory()
+inst.lb_eval_host_ptr(h_pf.data_ptr(), pf.shape[1], h_dp.data_ptr(), len(dp), h_lb.data_ptr())
+print("host gather", int(h_lb.sum().item()), flush=True)
 print("sanitize workload done")
