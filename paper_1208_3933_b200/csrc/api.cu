@@ -166,14 +166,14 @@ static int eval_host_gather(const fsp_instance *inst, HostCtx *c, const uint16_t
                             const int32_t *hd, int64_t pool, int32_t *lb_out)
 {
     const fsp_lb_plan &pl = inst->plan;
-    const int gather_sms = getenv("FSP_GATHER_SMS") ? atoi(getenv("FSP_GATHER_SMS")) : 8;
+    const int gather_sms = std::max(1, getenv("FSP_GATHER_SMS") ? atoi(getenv("FSP_GATHER_SMS")) : 8);
     const int lb_grid = std::max(1, pl.num_sms - gather_sms) * pl.ctas_per_sm;
     const int64_t tile = 32 * pl.npl;
     // chunks of one wave of tiles on the bounding SMs (no couple split); the
     // first ones are a quarter and a half wave, so the bounding starts after a
     // short gather that nothing overlaps
     const int64_t wave = (int64_t)lb_grid * pl.warps * tile;
-    const int64_t chunk = getenv("FSP_HOST_CHUNK") ? atoll(getenv("FSP_HOST_CHUNK")) : wave;
+    const int64_t chunk = std::max<int64_t>(tile, getenv("FSP_HOST_CHUNK") ? atoll(getenv("FSP_HOST_CHUNK")) : wave);
     const bool ramp = !getenv("FSP_HOST_NORAMP");
     auto chunk_of = [&](int64_t q) {
         return !ramp ? chunk : q == 0 ? std::max<int64_t>(tile, chunk / 4) : q == 1 ? std::max<int64_t>(tile, chunk / 2) : chunk;
@@ -220,10 +220,12 @@ static int eval_host_gather(const fsp_instance *inst, HostCtx *c, const uint16_t
         if (e == cudaSuccess) e = cudaStreamWaitEvent(ls, c->ev[s], 0);
         if (e != cudaSuccess) return fsp_cuda_fail(e, "gather");
         // (FSP_GATHER_ONLY: diagnostics, the transfers without the bounding)
+        // the last chunk has no gather to overlap: every SM bounds it
+        const bool last = off + cnt == pool && !getenv("FSP_HOST_LASTSPLIT");
         int rc = getenv("FSP_GATHER_ONLY") ? FSP_OK
                                            : fsp_launch_lb_dev(inst, c->d_pf[s], stride, c->d_dp[s], cnt,
                                                                nullptr, nullptr, 0, false, c->d_lb[s], ls,
-                                                               lb_grid);
+                                                               last ? 0 : lb_grid);
         if (rc != FSP_OK) return rc;
         e = cudaMemcpyAsync(lb_out + off, c->d_lb[s], sizeof(int32_t) * (size_t)cnt, cudaMemcpyDeviceToHost, ls);
         if (e == cudaSuccess) e = cudaEventRecord(c->ev_done[s], ls);
