@@ -579,6 +579,10 @@ def main():
         rate, cores, S, dt = cpu_oracle_rate(ptm, pf, dp, a.cpu_seconds)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"first {S} nodes of the rank-0 D1 pool ({dt:.1f} s on {cores} threads)"}
+        # the oracle on ONE core too (the paper's Tcpu)
+        r1, _, S1, dt1 = cpu_oracle_rate(ptm, pf, dp, max(1.0, a.cpu_seconds / 4), threads=1)
+        cpu["one_core"] = {"value": r1, "cores": 1,
+                           "sample": f"first {S1} nodes ({dt1:.1f} s on 1 thread)"}
 
     if rank == 0:
         cfgd = workload(cfg, a.pool, world)
