@@ -70,6 +70,8 @@ struct BBState {
     Nodes st, kp, ch;     // stack, kept parents (scratch), children
     unsigned long long *ch_key; // per child: (idle << 12) | j (R19 tie key)
     uint16_t *ch_uf;      // per child: its unscheduled jobs (n - depth entries, stride)
+    uint16_t *ppf;        // lazy rows (with ch_uf): the popped parents' rows [kcap][stride]
+    int32_t *ch_par;      // lazy rows: child -> parent index in the batch
     int32_t *ord;         // child slot -> child record, siblings by descending (LB, key)
     int32_t *d_maxnp;     // largest |S| among this iteration's expanded parents
     int32_t *d_famflag;   // 1: the family kernel bounds this iteration's children
@@ -228,6 +230,37 @@ __global__ void route_kernel(const int32_t *maxnp, const int64_t *count, int fam
     *count_sparse = fam ? 0 : *count;
 }
 
+// uint4 q of child row = its parent's row (d entries) with job x at position d
+// (rows padded with 0xffff); rows are 16-byte aligned (stride multiple of 8).
+__device__ __forceinline__ uint4 child_vec(const uint4 *prow4, int d, int x, int q)
+{
+    const int d8 = (d + 7) >> 3;
+    uint4 v = q < d8 ? prow4[q] : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    if (q == (d >> 3)) {
+        uint32_t *w4 = reinterpret_cast<uint32_t *>(&v);
+        const int t8 = d & 7;
+        uint32_t &wd = w4[t8 >> 1];
+        wd = (t8 & 1) ? ((wd & 0xffffu) | ((uint32_t)x << 16)) : ((wd & 0xffff0000u) | (uint32_t)x);
+    }
+    return v;
+}
+
+// Child prefix rows on demand (lazy mode: expand keeps the parents' rows
+// only; the bounding reads unscheduled lists): debug hook.
+__global__ void materialize_kernel(const uint16_t *__restrict__ ppf, const int32_t *__restrict__ ch_par,
+                                   const unsigned long long *__restrict__ ch_key, const int32_t *__restrict__ cdp,
+                                   int64_t cnt, int stride, uint16_t *cpf)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < cnt; c += warps) {
+        const int d = cdp[c] - 1, x = (int)(ch_key[c] & 0xfffu);
+        const uint4 *prow4 = reinterpret_cast<const uint4 *>(ppf + (size_t)ch_par[c] * stride);
+        uint4 *crow4 = reinterpret_cast<uint4 *>(cpf + (size_t)c * stride);
+        for (int q = lane; q < (stride >> 3); q += 32) crow4[q] = child_vec(prow4, d, x, q);
+    }
+}
+
 // Branching (a7): one warp per parent; its unscheduled jobs of ascending
 // (idle, j) rank cur .. cur+g-1 (R19) become children prefix + j;
 // lane t < g owns child t.  Child completion times C'_0 = C_0 + p_j0, C'_k = max(C'_k-1, C_k) + p_jk
@@ -236,7 +269,8 @@ __global__ void route_kernel(const int32_t *maxnp, const int64_t *count, int fam
 // Rows are 16-byte aligned (stride is a multiple of 8): copies move uint4s.
 __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t *__restrict__ off,
                               Nodes ch, unsigned long long *ch_key, uint16_t *ch_uf, Nodes kp,
-                              const int32_t *__restrict__ ptm, int n, int m, int stride, int by_idle)
+                              const int32_t *__restrict__ ptm, int n, int m, int stride, int by_idle,
+                              uint16_t *ppf, int32_t *ch_par)
 {
     extern __shared__ unsigned long long ex_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -340,21 +374,19 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
                 }
             }
             __syncwarp(); // keys are rewritten by the warp's next parent
-            // prefixes: every child row = the parent's row with its job at d
-            for (int t = 0; t < g; ++t) {
-                const int j = __shfl_sync(0xffffffffu, myj, t);
-                uint4 *crow4 = reinterpret_cast<uint4 *>(ch.pf + (size_t)(c0 + t) * stride);
-                for (int q = lane; q <= (d >> 3) && q < s8; q += 32) {
-                    uint4 v = q < d8 ? row4[q] : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu,
-                                                           0xffffffffu);
-                    if (q == (d >> 3)) { // insert j at position d
-                        uint32_t *w4 = reinterpret_cast<uint32_t *>(&v);
-                        const int t8 = d & 7;
-                        uint32_t &wd = w4[t8 >> 1];
-                        wd = (t8 & 1) ? ((wd & 0xffffu) | ((uint32_t)j << 16))
-                                      : ((wd & 0xffff0000u) | (uint32_t)j);
-                    }
-                    crow4[q] = v;
+            if (ppf) {
+                // lazy rows: keep the parent's row once; a child's row (parent +
+                // its job) is built only if it survives (scatter) or is the best
+                // leaf (commit) — most children are pruned right after bounding
+                uint4 *prow4 = reinterpret_cast<uint4 *>(ppf + (size_t)p * stride);
+                for (int q = lane; q < d8; q += 32) prow4[q] = row4[q];
+                if (lane < g) ch_par[c0 + lane] = (int32_t)p;
+            } else {
+                // prefixes: every child row = the parent's row with its job at d
+                for (int t = 0; t < g; ++t) {
+                    const int j = __shfl_sync(0xffffffffu, myj, t);
+                    uint4 *crow4 = reinterpret_cast<uint4 *>(ch.pf + (size_t)(c0 + t) * stride);
+                    for (int q = lane; q <= (d >> 3) && q < s8; q += 32) crow4[q] = child_vec(row4, d, j, q);
                 }
             }
             // completion times, lane t for child t: C'_0 = C_0 + p_j0,
@@ -491,7 +523,9 @@ __global__ void __launch_bounds__(kPruneThreads)
 __global__ void __launch_bounds__(kPruneThreads)
     scatter_kernel(Nodes ch, const int32_t *__restrict__ ord, const int64_t *count,
                    const int64_t *off_B, int n, int m, int stride, const int32_t *inc_dev,
-                   const int64_t *__restrict__ boff, int64_t first, Nodes st)
+                   const int64_t *__restrict__ boff, int64_t first, Nodes st,
+                   const uint16_t *__restrict__ ppf, const int32_t *__restrict__ ch_par,
+                   const unsigned long long *__restrict__ ch_key)
 {
     __shared__ int64_t s_dst[kPruneThreads];
     __shared__ int64_t s_src[kPruneThreads];
@@ -533,8 +567,12 @@ __global__ void __launch_bounds__(kPruneThreads)
             if (k < tot) {
                 src[u] = s_src[k];
                 dst[u] = s_dst[k];
-                d8[u] = (ch.dp[src[u]] + 7) >> 3;
-                if (lane < d8[u]) v[u] = reinterpret_cast<const uint4 *>(ch.pf + (size_t)src[u] * stride)[lane];
+                const int dc = ch.dp[src[u]];
+                d8[u] = (dc + 7) >> 3;
+                if (lane < d8[u])
+                    v[u] = ppf ? child_vec(reinterpret_cast<const uint4 *>(ppf + (size_t)ch_par[src[u]] * stride),
+                                           dc - 1, (int)(ch_key[src[u]] & 0xfffu), lane)
+                               : reinterpret_cast<const uint4 *>(ch.pf + (size_t)src[u] * stride)[lane];
                 if (lane < m) cv[u] = ch.C[(size_t)src[u] * m + lane];
             }
         }
@@ -544,7 +582,10 @@ __global__ void __launch_bounds__(kPruneThreads)
             uint4 *drow = reinterpret_cast<uint4 *>(st.pf + (size_t)dst[u] * stride);
             const uint4 *srow = reinterpret_cast<const uint4 *>(ch.pf + (size_t)src[u] * stride);
             if (lane < d8[u]) drow[lane] = v[u];
-            for (int q = lane + 32; q < d8[u]; q += 32) drow[q] = srow[q]; // rows beyond 256 jobs
+            for (int q = lane + 32; q < d8[u]; q += 32) // rows beyond 256 jobs
+                drow[q] = ppf ? child_vec(reinterpret_cast<const uint4 *>(ppf + (size_t)ch_par[src[u]] * stride),
+                                          ch.dp[src[u]] - 1, (int)(ch_key[src[u]] & 0xfffu), q)
+                              : srow[q];
             if (lane < m) st.C[(size_t)dst[u] * m + lane] = cv[u];
             for (int q = lane + 32; q < m; q += 32) st.C[(size_t)dst[u] * m + q] = ch.C[(size_t)src[u] * m + q];
         }
@@ -554,7 +595,8 @@ __global__ void __launch_bounds__(kPruneThreads)
 // Adopt the best leaf of this iteration (a8) and publish the status.
 __global__ void commit_kernel(Nodes ch, int n, int stride, int32_t *inc, unsigned long long *cand,
                               int32_t *perm, long long *packed, int rank, const int64_t *off_B,
-                              const int64_t *T_dev, BBStatus *status)
+                              const int64_t *T_dev, BBStatus *status, const uint16_t *ppf,
+                              const int32_t *ch_par, const unsigned long long *ch_key)
 {
     __shared__ int s_improved;
     __shared__ uint32_t s_bm[FSP_MAX_JOBS / 32];
@@ -565,13 +607,15 @@ __global__ void commit_kernel(Nodes ch, int n, int stride, int32_t *inc, unsigne
         const int mk = (int)(c >> 32);
         const int64_t idx = (int64_t)(c & 0xffffffffull);
         if (mk < *inc) {
-            const uint16_t *row = ch.pf + (size_t)idx * stride;
+            // the leaf's row: its own, or (lazy rows) its parent's + its job
+            const uint16_t *row = ppf ? ppf + (size_t)ch_par[idx] * stride : ch.pf + (size_t)idx * stride;
             const int d = ch.dp[idx];
             for (int w = threadIdx.x; w < (n + 31) / 32; w += blockDim.x) s_bm[w] = 0;
             __syncthreads();
             for (int i = threadIdx.x; i < d; i += blockDim.x) {
-                perm[i] = row[i];
-                atomicOr(&s_bm[row[i] >> 5], 1u << (row[i] & 31));
+                const int j = ppf && i == d - 1 ? (int)(ch_key[idx] & 0xfffu) : row[i];
+                perm[i] = j;
+                atomicOr(&s_bm[j >> 5], 1u << (j & 31));
             }
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -624,6 +668,8 @@ void bb_free(BBState *s)
     free_nodes(s->ch);
     cudaFree(s->ch_key);
     cudaFree(s->ch_uf);
+    cudaFree(s->ppf);
+    cudaFree(s->ch_par);
     cudaFree(s->ord);
     cudaFree(s->d_maxnp);
     cudaFree(s->d_famflag);
@@ -811,7 +857,7 @@ int bb_iterate(BBState *s)
     const size_t esmem = (size_t)ewarps * 8 * (n + ((n + 31) / 32 + 1) / 2 + 16);
     expand_kernel<<<eblocks, ewarps * 32, esmem, st>>>(s->st, first, B, s->off, s->ch, s->ch_key,
                                                        s->ch_uf, s->kp, inst->d_ptm32, n, m, stride,
-                                                       s->order);
+                                                       s->order, s->ppf, s->ch_par);
     const int64_t *off_B = s->off + B; // (kept << 32) | children, on the device
     // bounding (before the kept parents overwrite the popped range): the
     // family kernel from the parents (one of the two launches exits at once),
@@ -839,9 +885,11 @@ int bb_iterate(BBState *s)
                                                   s->bcnt, s->d_stats);
     device_scan(s, nullptr, s->bcnt, nblk, s->boff, nullptr);
     scatter_kernel<<<nblk, kPruneThreads, 0, st>>>(s->ch, s->ord, s->d_count, off_B, n, m, stride,
-                                                    s->d_inc, s->boff, first, s->st);
+                                                    s->d_inc, s->boff, first, s->st, s->ppf, s->ch_par,
+                                                    s->ch_key);
     commit_kernel<<<1, 256, 0, st>>>(s->ch, n, stride, s->d_inc, s->d_cand, s->d_perm, s->d_packed,
-                                     s->rank, off_B, s->boff + nblk, s->d_status);
+                                     s->rank, off_B, s->boff + nblk, s->d_status, s->ppf, s->ch_par,
+                                     s->ch_key);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && s->timing) e = cudaEventRecord(s->ev_t1, st);
     if (e == cudaSuccess)
@@ -925,8 +973,15 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     alloc((void **)&s->ch_key, (size_t)s->ccap * 8);
     // unscheduled lists for the sparse byte-row bounding plan (long prefixes:
     // deep children have n' << d); measured slower for n < 64 (dense plan)
-    if (env_i64("FSP_BB_ULIST", 1) != 0 && inst->plan_bb.sparse && inst->plan_bb.byte_rows)
+    if (env_i64("FSP_BB_ULIST", 1) != 0 && inst->plan_bb.sparse && inst->plan_bb.byte_rows) {
         alloc((void **)&s->ch_uf, (size_t)s->ccap * s->stride * 2);
+        // the bounding then reads no child prefix: rows are built only for
+        // the survivors and the best leaf (FSP_BB_LAZY=0: every child's row)
+        if (env_i64("FSP_BB_LAZY", 1) != 0) {
+            alloc((void **)&s->ppf, (size_t)s->kcap * s->stride * 2);
+            alloc((void **)&s->ch_par, (size_t)s->ccap * 4);
+        }
+    }
     alloc((void **)&s->ord, (size_t)s->ccap * 4);
     alloc((void **)&s->d_maxnp, 4);
     alloc((void **)&s->d_famflag, 4);
@@ -1105,6 +1160,12 @@ extern "C" int fsp_bb_debug_children(void *state, int64_t max_nodes, void *h_buf
     const int64_t k = std::min(max_nodes, s->last_children);
     *n_out = k;
     if (k == 0) return FSP_OK;
+    if (s->ppf) { // lazy rows: build the children's prefixes first
+        materialize_kernel<<<(unsigned)std::min<int64_t>((k + 7) / 8, 148 * 16), 256, 0, s->stream>>>(
+            s->ppf, s->ch_par, s->ch_key, s->ch.dp, k, s->stride, s->ch.pf);
+        cudaError_t e0 = cudaGetLastError();
+        if (e0 != cudaSuccess) return fsp_cuda_fail(e0, "debug children");
+    }
     uint8_t *b = static_cast<uint8_t *>(h_buf);
     const size_t pfb = (size_t)k * s->stride * 2, cb = (size_t)k * s->m * 4;
     cudaStream_t q = s->stream;

@@ -1466,7 +1466,9 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.dbg_skip = getenv("FSP_LB_DEBUG_SKIP") ? atoi(getenv("FSP_LB_DEBUG_SKIP")) : 0;
     a.lane_ingest = getenv("FSP_LB_LANE_INGEST") ? atoi(getenv("FSP_LB_LANE_INGEST")) : 1;
     // unscheduled lists: byte-row plans with supplied completion times only
-    a.ulist = ulist && cin && pl.s16 && pl.maxm >= 10 && pl.byte_rows && a.lane_ingest ? ulist : nullptr;
+    // (the B&B's lazy child rows rely on this: with a list, no prefix is read)
+    a.ulist = ulist && cin && pl.s16 && pl.maxm >= 10 && pl.byte_rows ? ulist : nullptr;
+    if (a.ulist) a.lane_ingest = 1;
     a.prof = nullptr;
     static unsigned long long *prof_buf = nullptr; // diagnostics only (FSP_LB_PROF=1)
     const bool prof = getenv("FSP_LB_PROF") && atoi(getenv("FSP_LB_PROF")) != 0;
