@@ -87,6 +87,7 @@ extern "C" int fsp_check(const fsp_instance *inst, void *cuda_stream)
 struct HostCtx {
     std::mutex mu;
     cudaStream_t st[2] = {nullptr, nullptr};
+    cudaStream_t st2 = nullptr; // gather path: second bounding stream (consecutive chunks' launches overlap their tails)
     int64_t cap_nodes = 0;
     int32_t cap_stride = 0;
     uint16_t *d_pf[2] = {nullptr, nullptr};
@@ -99,6 +100,7 @@ struct HostCtx {
 void fsp_host_ctx_free(void *p)
 {
     HostCtx *c = static_cast<HostCtx *>(p);
+    if (c->st2) cudaStreamDestroy(c->st2);
     for (int s = 0; s < 2; ++s) {
         if (c->st[s]) cudaStreamDestroy(c->st[s]);
         cudaFree(c->d_pf[s]);
@@ -204,7 +206,16 @@ static int eval_host_gather(const fsp_instance *inst, HostCtx *c, const uint16_t
             if (e != cudaSuccess) return fsp_cuda_fail(e, "event create");
         }
     }
+    if (!c->st2) {
+        cudaError_t e = cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return fsp_cuda_fail(e, "stream create");
+    }
+    // buffer s is bounded on stream lss[s]: chunk q+1's launch can start on the
+    // SMs that chunk q's launch has already left (one stream would serialise
+    // them, leaving every chunk's tail wave idle)
     cudaStream_t gs = c->st[1], ls = c->st[0];
+    const bool two = !getenv("FSP_HOST_ONE_LB_STREAM");
+    cudaStream_t lss[2] = {c->st[0], two ? c->st2 : c->st[0]};
     int64_t off = 0;
     for (int64_t q = 0; off < pool; ++q) {
         const int s = (int)(q & 1);
@@ -217,22 +228,24 @@ static int eval_host_gather(const fsp_instance *inst, HostCtx *c, const uint16_t
             e = cudaGetLastError();
         }
         if (e == cudaSuccess) e = cudaEventRecord(c->ev[s], gs);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(ls, c->ev[s], 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(lss[s], c->ev[s], 0);
         if (e != cudaSuccess) return fsp_cuda_fail(e, "gather");
         // (FSP_GATHER_ONLY: diagnostics, the transfers without the bounding)
         // the last chunk has no gather to overlap: every SM bounds it
         const bool last = off + cnt == pool && !getenv("FSP_HOST_LASTSPLIT");
         int rc = getenv("FSP_GATHER_ONLY") ? FSP_OK
                                            : fsp_launch_lb_dev(inst, c->d_pf[s], stride, c->d_dp[s], cnt,
-                                                               nullptr, nullptr, 0, false, c->d_lb[s], ls,
+                                                               nullptr, nullptr, 0, false, c->d_lb[s], lss[s],
                                                                last ? 0 : lb_grid);
         if (rc != FSP_OK) return rc;
-        e = cudaMemcpyAsync(lb_out + off, c->d_lb[s], sizeof(int32_t) * (size_t)cnt, cudaMemcpyDeviceToHost, ls);
-        if (e == cudaSuccess) e = cudaEventRecord(c->ev_done[s], ls);
+        e = cudaMemcpyAsync(lb_out + off, c->d_lb[s], sizeof(int32_t) * (size_t)cnt, cudaMemcpyDeviceToHost,
+                            lss[s]);
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_done[s], lss[s]);
         if (e != cudaSuccess) return fsp_cuda_fail(e, "D2H");
         off += cnt;
     }
-    cudaError_t e = cudaStreamSynchronize(ls);
+    cudaError_t e = cudaStreamSynchronize(lss[0]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(lss[1]);
     if (e == cudaSuccess) e = cudaStreamSynchronize(gs);
     if (e != cudaSuccess) return fsp_cuda_fail(e, "sync");
     return fsp_check(inst, ls);
