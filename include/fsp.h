@@ -95,6 +95,7 @@ typedef struct {
     int32_t sparse_walk;      /* 1: walk over the block's live jobs only      */
     int32_t smem_bytes;
     int32_t tail_split;       /* split of the last, partial tile iteration    */
+    int32_t heads_jp;         /* 1: heads/tails/loads by job pairs (16x2 ops) */
 } fsp_lb_launch;
 
 int fsp_lb_launch_info(const fsp_instance *inst, int64_t pool, int32_t sibling,

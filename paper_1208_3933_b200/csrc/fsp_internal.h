@@ -59,6 +59,9 @@ struct fsp_lb_plan {
     int pairs_per_group; // couples per group (last group may be shorter)
     int dbuf;            // couple-group buffers in shared memory (0: one + CTA barrier)
     bool byte_rows;      // 16-bit walk, m >= 10: U rows of one byte per lane (else nibbles)
+    bool jp;             // dense TM plans: job-pair heads (PTM + job-pair rows staged, no pq
+                         //   rows; lb_kernel.cu jp_heads), jp_m = the masking offset M
+    int jp_m;
     bool recs_global;    // ablation: couple records read from global memory (20-machine dense)
     int warps;           // warps per CTA
     int ctas_per_sm;
@@ -84,7 +87,8 @@ struct fsp_instance {
     int32_t *h_ptm;
     // device tables
     uint8_t *d_tables;   // groups * group_bytes: per group [pairs][n] fsp_rec then u32 couple ids
-    int32_t *d_ptm32s;   // [n][mp4] int32, padded rows (lb kernel smem image)
+    int32_t *d_ptm32s;   // [n][mp4] int32, padded rows + per-plan rows (lb kernel smem image, plan)
+    int32_t *d_ptm32s_bb; // the same for plan_bb
     int32_t *d_ptm32;    // [n][m] int32 (B&B)
     int *d_err;          // malformed-node flag
     int64_t table_bytes;

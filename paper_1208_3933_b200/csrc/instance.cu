@@ -87,6 +87,37 @@ static void build_tables(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl
     }
 }
 
+// Shared-memory image of PTM for plan `pl`: int32 rows padded to mp4 (16-byte
+// rows), then, TMEM plans, either the job-pair rows (pl.jp: row i, word k =
+// p_{2i,k} | p_{2i+1,k} << 16, job n = 0) or the packed (p, q) machine-pair
+// rows (fsp_pq_words).
+static std::vector<int32_t> ptm_image(const int32_t *ptm, int n, int m, const fsp_lb_plan &pl)
+{
+    const int mp4 = (m + 3) & ~3;
+    std::vector<int32_t> p32(pl.L.ptm_bytes / 4, 0);
+    for (int j = 0; j < n; ++j)
+        for (int k = 0; k < m; ++k) p32[(size_t)j * mp4 + k] = ptm[(size_t)j * m + k];
+    if (pl.jp) {
+        uint32_t *jp = reinterpret_cast<uint32_t *>(p32.data() + (size_t)n * mp4);
+        for (int j = 0; j < n; ++j)
+            for (int k = 0; k < m; ++k)
+                jp[(size_t)(j / 2) * mp4 + k] |= (uint32_t)ptm[(size_t)j * m + k] << (16 * (j & 1));
+    } else if (pl.s16 && pl.maxm >= 10) { // nibble/TMEM variants: packed (p, q) machine pairs
+        const int W = fsp_pq_words(pl.maxm), H = W / 2;
+        uint32_t *pq = reinterpret_cast<uint32_t *>(p32.data() + (size_t)n * mp4);
+        for (int j = 0; j < n; ++j) {
+            std::vector<int32_t> pj(pl.maxm + 1, 0), qj(pl.maxm + 1, 0);
+            for (int k = 0; k < m; ++k) pj[k] = ptm[(size_t)j * m + k];
+            for (int l = m - 2; l >= 0; --l) qj[l] = qj[l + 1] + pj[l + 1]; // q_jl = sum_{i>l} p_ji
+            for (int kp = 0; 2 * kp < m; ++kp) {
+                pq[(size_t)j * W + kp] = (uint32_t)pj[2 * kp] | ((uint32_t)pj[2 * kp + 1] << 16);
+                pq[(size_t)j * W + H + kp] = (uint32_t)qj[2 * kp] | ((uint32_t)qj[2 * kp + 1] << 16);
+            }
+        }
+    }
+    return p32;
+}
+
 extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_instance **out)
 {
     if (!ptm || !out) return fsp_fail(FSP_EINVAL, "null pointer");
@@ -132,24 +163,8 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
     build_tables(ptm, n, m, inst->plan, blob);
     build_tables(ptm, n, m, inst->plan_bb, blob_bb);
 
-    // ---- PTM as int32 rows padded to mp4 (16-byte rows) for shared memory ----
-    const int mp4 = (m + 3) & ~3;
-    std::vector<int32_t> p32(pl.L.ptm_bytes / 4, 0);
-    for (int j = 0; j < n; ++j)
-        for (int k = 0; k < m; ++k) p32[(size_t)j * mp4 + k] = ptm[(size_t)j * m + k];
-    if (pl.s16 && pl.maxm >= 10) { // nibble/TMEM variants: packed (p, q) machine pairs
-        const int W = fsp_pq_words(pl.maxm), H = W / 2;
-        uint32_t *pq = reinterpret_cast<uint32_t *>(p32.data() + (size_t)n * mp4);
-        for (int j = 0; j < n; ++j) {
-            std::vector<int32_t> pj(pl.maxm + 1, 0), qj(pl.maxm + 1, 0);
-            for (int k = 0; k < m; ++k) pj[k] = ptm[(size_t)j * m + k];
-            for (int l = m - 2; l >= 0; --l) qj[l] = qj[l + 1] + pj[l + 1]; // q_jl = sum_{i>l} p_ji
-            for (int kp = 0; 2 * kp < m; ++kp) {
-                pq[(size_t)j * W + kp] = (uint32_t)pj[2 * kp] | ((uint32_t)pj[2 * kp + 1] << 16);
-                pq[(size_t)j * W + H + kp] = (uint32_t)qj[2 * kp] | ((uint32_t)qj[2 * kp + 1] << 16);
-            }
-        }
-    }
+    const std::vector<int32_t> p32 = ptm_image(ptm, n, m, inst->plan);
+    const std::vector<int32_t> p32bb = ptm_image(ptm, n, m, inst->plan_bb);
 
     inst->table_bytes = (int64_t)blob.size();
     e = cudaMalloc(&inst->d_tables, blob.size());
@@ -157,6 +172,9 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
     if (e == cudaSuccess)
         e = cudaMemcpy(inst->d_tables_bb, blob_bb.data(), blob_bb.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&inst->d_ptm32s, pl.L.ptm_bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&inst->d_ptm32s_bb, inst->plan_bb.L.ptm_bytes);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(inst->d_ptm32s_bb, p32bb.data(), inst->plan_bb.L.ptm_bytes, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&inst->d_ptm32, sizeof(int32_t) * (size_t)n * m);
     if (e == cudaSuccess) e = cudaMalloc(&inst->d_err, sizeof(int));
     if (e == cudaSuccess)
@@ -188,6 +206,7 @@ extern "C" void fsp_instance_free(fsp_instance *inst)
     if (inst->d_tables) cudaFree(inst->d_tables);
     if (inst->d_tables_bb) cudaFree(inst->d_tables_bb);
     if (inst->d_ptm32s) cudaFree(inst->d_ptm32s);
+    if (inst->d_ptm32s_bb) cudaFree(inst->d_ptm32s_bb);
     if (inst->d_ptm32) cudaFree(inst->d_ptm32);
     if (inst->d_err) cudaFree(inst->d_err);
     if (inst->d_fam) cudaFree(inst->d_fam);
@@ -238,5 +257,6 @@ extern "C" int fsp_lb_launch_info(const fsp_instance *inst, int64_t pool, int32_
     out->sparse_walk = pl.sparse ? 1 : 0;
     out->smem_bytes = (int32_t)pl.smem_bytes;
     out->tail_split = sibling ? 1 : fsp_lb_tail_split(pl, pool, split);
+    out->heads_jp = pl.jp ? 1 : 0;
     return FSP_OK;
 }

@@ -199,8 +199,12 @@ struct LbArgs {
                            // lane SETS its node's bits (deep nodes: n' << d entries)
     int lane_ingest;       // scheduled-set build with one node per lane (byte and
                            // lane-major rows); 0: the warp-per-node pass
+    int jp;                // job-pair heads (fsp_lb_plan::jp): s_pq holds the job-pair rows
+    uint32_t jp_m;         // their masking offset M (multiple of 16)
+    uint32_t one;          // 1 (a multiplier ptxas keeps on the FMA pipe)
     int dbg_skip;          // diagnostics only (FSP_LB_DEBUG_SKIP): bit 0 skips the
-                           // per-node heads phase, bit 1 the couple walks (LBs wrong)
+                           // per-node heads phase, bit 1 the couple walks, bit 2 the
+                           // job-pair heads (C pass only), bit 3 the C pass (LBs wrong)
 };
 
 // FSP_LB_PROF phases: cycles lane 0 of every warp spends in each part
@@ -317,6 +321,95 @@ __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1
                 upd<S16>((MASK).b[q_], lanebit, (C1), x_, ee[q_]);              \
         }                                                                       \
     }
+
+// Rows a2/a3 of one node (lane's node q) over job PAIRS (2i, 2i+1), dense TMEM
+// plans (fsp_lb_plan::jp).  Each 16x2 op carries both jobs of a pair for the
+// node: job 2i in the low half, 2i+1 in the high half.  A scheduled job's half
+// starts at M (a multiple of 16 above every real head and tail, host-checked
+// with M + sum_k p_jk <= 65535), so it never wins a minimum and no branch or
+// predicate is needed:
+//   r_j0 = max(C_0, M2),  r_jk = max(C_k, r_j,k-1 + p_j,k-1)   (R3)   -> RR_k = min
+//   t_j,m-1 = M2,  t_jl = t_j,l+1 + p_j,l+1  (= q_jl + M2, R4)       -> QQ_l = min
+//   L_k = sum p_jk over unscheduled j: one multiply-add per machine with the
+//   swapped flags (a_hi | a_lo << 16) x (p_lo | p_hi << 16), whose high half
+//   is a_hi p_hi + a_lo p_lo (the low half collects <= ceil(n/2) max p, host-
+//   checked against a carry)
+// Per pair: 2 x m - 1 ALU ops for the heads, m - 1 for the tails, ~4 for the
+// flags; the loads' and the tails' running sums are FMA-pipe multiply-adds.
+// Returns true for a malformed node (unscheduled count != n - depth).
+template <int MAXM, int HM, int NPLP, class UL>
+__device__ __forceinline__ bool jp_heads(const LbArgs &a, const uint32_t *s_jp, const uint32_t *Uw,
+                                         int urow, int useg, int lane, int q, const int (&C)[MAXM],
+                                         uint32_t tbase, int n, int want)
+{
+    constexpr int MP4 = (MAXM + 3) & ~3;
+    uint32_t C2[MAXM], RR[MAXM], QQ[MAXM], LL[MAXM];
+#pragma unroll
+    for (int k = 0; k < MAXM; ++k) {
+        C2[k] = (uint32_t)C[k] * 0x10001u;
+        RR[k] = QQ[k] = 0xffffffffu;
+        LL[k] = 0u;
+    }
+    const uint32_t M = a.jp_m, MM = M * 0x10001u, one = a.one;
+    const int sh = UL::bit(lane, q);
+    const uint32_t *uw = Uw + useg + UL::word(lane, q);
+    uint32_t cnt2 = 0;
+    const int npair = (n + 1) >> 1; // row n of U is the always-empty padding row
+#pragma unroll 1
+    for (int i = 0; i < npair; ++i) {
+        const uint32_t xl = uw[(2 * i) * urow], xh = uw[(2 * i + 1) * urow];
+        const uint32_t bl = (xl >> sh) & 1u, bh = (xh >> sh) & 1u;
+        const uint32_t ab = bl | (bh << 16), absw = bh | (bl << 16);
+        const uint32_t M2 = MM - ab * M;
+        cnt2 += ab;
+        const uint4 *pr = reinterpret_cast<const uint4 *>(s_jp + (size_t)i * MP4);
+        uint32_t pw[MP4];
+#pragma unroll
+        for (int k4 = 0; k4 < MP4 / 4; ++k4) {
+            const uint4 v = pr[k4];
+            pw[4 * k4] = v.x;
+            pw[4 * k4 + 1] = v.y;
+            pw[4 * k4 + 2] = v.z;
+            pw[4 * k4 + 3] = v.w;
+        }
+        uint32_t r = __vmaxu2(C2[0], M2);
+        RR[0] = __vminu2(RR[0], r);
+#pragma unroll
+        for (int k = 1; k < MAXM; ++k) {
+            r = __viaddmax_u16x2(r, pw[k - 1], C2[k]);
+            RR[k] = __vminu2(RR[k], r);
+        }
+        uint32_t t = M2;
+#pragma unroll
+        for (int l = MAXM - 2; l >= 0; --l) {
+            QQ[l] = __viaddmin_u16x2(t, pw[l + 1], QQ[l]);
+            t = pw[l + 1] * one + t;
+        }
+#pragma unroll
+        for (int k = 0; k < MAXM; ++k) LL[k] = pw[k] * absw + LL[k];
+    }
+    const int cnt = (int)((cnt2 & 0xffffu) + (cnt2 >> 16));
+    uint32_t R2[HM], A2[HM], Q2[HM];
+#pragma unroll
+    for (int kp = 0; kp < HM; ++kp) {
+        const uint32_t r0 = RR[2 * kp], r1 = RR[2 * kp + 1];
+        const uint32_t q0 = QQ[2 * kp], q1 = 2 * kp + 1 == MAXM - 1 ? 0u : QQ[2 * kp + 1];
+        R2[kp] = __vminu2(__byte_perm(r0, r1, 0x5410), __byte_perm(r0, r1, 0x7632));
+        Q2[kp] = __vminu2(__byte_perm(q0, q1, 0x5410), __byte_perm(q0, q1, 0x7632));
+        A2[kp] = R2[kp] + __byte_perm(LL[2 * kp], LL[2 * kp + 1], 0x7632); // A = R + L
+        if (cnt == 0) { // R6: complete schedule, R = C, A = C, Q = 0
+            R2[kp] = A2[kp] = __byte_perm(C2[2 * kp], C2[2 * kp + 1], 0x5410);
+            Q2[kp] = 0u;
+        }
+    }
+#pragma unroll
+    for (int kp = 0; kp < HM; ++kp) {
+        tm_st1(tbase + (0 * HM + kp) * NPLP + q, R2[kp]);
+        tm_st1(tbase + (1 * HM + kp) * NPLP + q, A2[kp]);
+        tm_st1(tbase + (2 * HM + kp) * NPLP + q, Q2[kp]);
+    }
+    return cnt != want;
+}
 
 // launch bounds: 8 warps for m > 20; 4 warps x 5 CTAs per SM for m = 5 (the
 // per-node phase dominates there: small CTAs, registers capped at 96 so five
@@ -685,6 +778,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                     }
                 }
             }
+            const uint32_t one = a.one;
             auto step = [&](uint32_t job) {
                 if (job >= (uint32_t)n) {
                     bad = true;
@@ -701,38 +795,43 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                         for (int t = 0; t < 4; ++t) {
                             const int k = 4 * k4 + t;
                             if (k < MAXM && k < m) {
-                                C[k] = max(C[k], prev) + pv[t];
+                                // max(C_k, C'_k-1) + p = max(C'_k-1 + p, C_k + p):
+                                // the second sum on the FMA pipe (one * p + C),
+                                // one VIADDMNMX on the ALU pipe
+                                C[k] = __viaddmax_s32(prev, pv[t], pv[t] * (int)one + C[k]);
                                 prev = C[k];
                             }
                         }
                     }
                 }
             };
-            const int dd = a.cin ? 0 : d;
+            const int dd = a.cin || (a.dbg_skip & 8) ? 0 : d;
             // fused ingest: also clear this node's bit of each scheduled job's
             // row (byte rows: lane-owned byte; lane-major: shared atomic)
             uint8_t *ubq = reinterpret_cast<uint8_t *>(Uw + useg) + lane;
-            auto step_clr = [&](uint32_t job) {
+            auto clr = [&](uint32_t job) {
                 if (fused && job < (uint32_t)n) {
                     if constexpr (UL::BYTES) ubq[job * (urow * 4)] &= (uint8_t)~(2u << q);
                     else atomicAnd(&Uw[job * urow + useg + q], ~lanebit);
                 }
+            };
+            auto step_clr = [&](uint32_t job) {
+                clr(job);
                 step(job);
             };
             int i = 0;
-            // 16-byte rows: eight job ids per vector load
+            // 16-byte rows: eight job ids per vector load; the eight clears
+            // follow the eight steps, so no shared store sits between a step's
+            // PTM-row loads and the previous step (the loads can be hoisted)
             if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
                 const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
                 for (; i + 8 <= dd; i += 8) {
                     const uint4 v = r4[i >> 3];
-                    step_clr(v.x & 0xffffu);
-                    step_clr(v.x >> 16);
-                    step_clr(v.y & 0xffffu);
-                    step_clr(v.y >> 16);
-                    step_clr(v.z & 0xffffu);
-                    step_clr(v.z >> 16);
-                    step_clr(v.w & 0xffffu);
-                    step_clr(v.w >> 16);
+                    const uint32_t w8[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) step(t & 1 ? w8[t >> 1] >> 16 : w8[t >> 1] & 0xffffu);
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) clr(t & 1 ? w8[t >> 1] >> 16 : w8[t >> 1] & 0xffffu);
                 }
             }
             for (; i < dd; ++i) step_clr(row[i]);
@@ -744,6 +843,15 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             // are < 2^15, host-checked): tails q_jl come from a per-job table of
             // machine pairs (one VIMNMX.U16x2 per pair) and p_jl from another
             // (one add per pair), next to PTM in shared memory
+            if constexpr (TM && !SPARSE && EXACT) {
+                if (a.jp && (a.dbg_skip & 4)) continue; // diagnostics: C pass only
+                if (a.jp) { // rows a2/a3 by job pairs (jp_heads), then the TMEM stores
+                    if (jp_heads<MAXM, HM, NPLP, UL>(a, s_pq, Uw, urow, useg, lane, q, C, tbase, n,
+                                                     node < pool ? n - d : 0))
+                        bad = true;
+                    continue;
+                }
+            }
             int R[MAXM], Q[MAXM], Ld[MAXM];
             uint32_t Q2[HM], L2[HM], R2[HM];
 #pragma unroll
@@ -1256,6 +1364,24 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     const int mp4 = (m + 3) & ~3;
     pl.nrec = (n + 3) & ~3; // walk steps of 4 positions
     pl.npl = 2;
+    // job-pair heads (dense TMEM plans, exact m): the heads, tails and loads of
+    // two jobs per 16x2 op, scheduled halves pushed above every real value by
+    // the offset M: needs M > (n+m)*max p (every real r_jk, q_jl) and
+    // M + sum_k p_jk <= 65535; the low halves of the packed loads collect
+    // ceil(n/2)*max p (see jp_heads in lb_kernel)
+    {
+        int64_t maxsum = 0;
+        for (int j = 0; j < n; ++j) {
+            int64_t sj = 0;
+            for (int k = 0; k < m; ++k) sj += inst->h_ptm[(size_t)j * m + k];
+            maxsum = std::max(maxsum, sj);
+        }
+        const int64_t M = (65535 - maxsum) & ~int64_t(15);
+        pl.jp_m = (int)std::max<int64_t>(M, 0);
+        pl.jp = !sparse && pl.exact && pl.s16 && m >= 10 && M > (int64_t)(n + m) * inst->max_p &&
+                (int64_t)((n + 1) / 2) * inst->max_p <= 65535;
+        if (const char *s = getenv("FSP_LB_JP")) pl.jp = pl.jp && atoi(s) != 0;
+    }
     // Candidates: nodes per lane (4 only for the exact-m specialisations), warps
     // per CTA, fewest couple groups that fit.  Score = resident warps per SM
     // (latency hiding) x 1.5 for 4 nodes per lane (half the table and mask
@@ -1292,7 +1418,9 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
             const int wpr = !nib ? npl : lay == 0 ? 8 : (32 + 31 / (npl + 1) - 1) / (31 / (npl + 1));
             // nibble: per-warp blocks of (n+1) rows of wpr|1 words (odd: the 32 jobs a
             // warp clears at once hit 32 banks); record offsets j*4*urow < 64 KB
-            const int urow = nib ? wpr | 1 : npl * W;
+            // (FSP_LB_UROW_PAD=0: byte rows unpadded, 8 words; measured below)
+            const bool pad = !getenv("FSP_LB_UROW_PAD") || atoi(getenv("FSP_LB_UROW_PAD")) != 0;
+            const int urow = nib ? (lay == 0 && !pad ? wpr : wpr | 1) : npl * W;
             if (!nib && (size_t)(n + 1) * 4 * urow > 65535) continue; // 16-bit U row offsets
             if (nib && (size_t)(n + 1) * 4 * urow > 65535) continue;
             fsp_lb_layout L{};
@@ -1300,7 +1428,10 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
             L.u_bytes = align16((size_t)(nib ? W : 1) * (n + 1) * 4 * urow);
             L.off_u = 0;
             // + the packed (p, q) machine-pair rows of the TM (nibble) variants
-            L.ptm_bytes = align16((size_t)n * mp4 * 4) + (nib ? (size_t)n * fsp_pq_words(pl.maxm) * 4 : 0);
+            // jp plans: + the job-pair rows [ceil(n/2)][mp4] (p_2i,k | p_2i+1,k << 16)
+            L.ptm_bytes = align16((size_t)n * mp4 * 4) +
+                          (pl.jp ? (size_t)((n + 1) / 2) * mp4 * 4
+                                 : nib ? (size_t)n * fsp_pq_words(pl.maxm) * 4 : 0);
             L.off_ptm = L.u_bytes;
             L.off_bar = L.off_ptm + L.ptm_bytes;
             // nibble variants keep R/A/Q in TMEM: ceil(W/4) blocks of 3*ceil(maxm/2)*npl
@@ -1435,7 +1566,10 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     const uint8_t *tables = sparse ? inst->d_tables_bb : inst->d_tables;
     LbArgs a;
     a.tables = tables;
-    a.ptm = inst->d_ptm32s;
+    a.ptm = sparse ? inst->d_ptm32s_bb : inst->d_ptm32s;
+    a.jp = pl.jp ? 1 : 0;
+    a.jp_m = (uint32_t)pl.jp_m;
+    a.one = 1u;
     a.cin = cin;
     a.cin_stride = cin_stride;
     // eight job ids per lane pay off only for long prefixes (measured: 20x5 and

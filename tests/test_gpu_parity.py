@@ -254,6 +254,43 @@ def test_parity_walk16_offset_boundary(torch, fsp, orc, n, m):
         assert inst.info["walk16"] == walk16
 
 
+@pytest.mark.parametrize("n,m", [(20, 20), (41, 10), (200, 20)])
+def test_parity_heads_job_pairs_boundary(torch, fsp, orc, n, m):
+    """Job-pair heads (lb_kernel.cu jp_heads) push a scheduled job's half to an
+    offset M = (65535 - max_j sum_k p_jk) rounded down to 16 and are taken iff
+    M > (n + m) * max p: instances at the largest admissible max p (every real
+    head, tail and load close to M) and one above it (per-job heads) both match
+    the oracle; odd n exercises the padding job of the last pair."""
+    def ok(p):
+        return ((65535 - m * p) & ~15) > (n + m) * p and ((n + 1) // 2) * p <= 65535
+    pmax = max(p for p in range(1, 4000) if ok(p))
+    for pm, jp in [(pmax, 1), (pmax + 1, 0)]:
+        rng = np.random.default_rng(3933 + n * m + pm)
+        ptm = rng.integers(pm // 2, pm + 1, size=(n, m)).astype(np.int32)
+        ptm[0, :] = pm  # one job at max p on every machine: the largest row sum
+        parts = [inputs.pool_d1(n, 2000, 977 + pm),
+                 inputs.pool_fixed_depth(n, 40, n, 978 + pm),  # complete schedules (R6)
+                 inputs.pool_fixed_depth(n, 40, n - 1, 979 + pm)]  # one unscheduled job
+        pf = np.concatenate([p[0] for p in parts])
+        dp = np.concatenate([p[1] for p in parts])
+        inst = compare(torch, fsp, orc, ptm, pf, dp)
+        assert inst.launch_info(len(dp))["heads_jp"] == jp
+
+
+@pytest.mark.parametrize("name", ["ta021", "ta091"])
+def test_heads_job_pairs_ab(torch, fsp, orc, monkeypatch, name):
+    """The same pool through the job-pair heads and the per-job heads
+    (FSP_LB_JP=0, the A/B switch) gives identical LBs, equal to the oracle's."""
+    n, m, seed = inputs.TAILLARD_SEEDS[name]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, 5000, inputs.pool_seed(name) + 5)
+    a = compare(torch, fsp, orc, ptm, pf, dp)
+    assert a.launch_info(len(dp))["heads_jp"] == 1
+    monkeypatch.setenv("FSP_LB_JP", "0")
+    b = compare(torch, fsp, orc, ptm, pf, dp)
+    assert b.launch_info(len(dp))["heads_jp"] == 0
+
+
 # ------------------------------------------- bench launch shapes (VERDICT r1)
 
 def _sampled(torch, fsp, orc, ptm, pf, dp, k, seed):

@@ -53,6 +53,18 @@ __global__ void __launch_bounds__(512) k(unsigned *out, unsigned x, unsigned y, 
                 else e[i] = __umulhi(e[i], x) + y;
             }
             if constexpr (V == 9) e[i] = __vimax3_u16x2(e[i], x, y);                  // VIMNMX3.U16x2
+            if constexpr (V == 13) e[i] = e[i] * xr + yr;                              // IMAD
+            if constexpr (V == 14) e[i] = __byte_perm(e[i], xr, 0x5410u + i);          // PRMT
+            if constexpr (V == 15) e[i] = __umulhi(e[i], xr) ^ (unsigned)i;            // IMAD.HI (+LOP3?)
+            if constexpr (V == 16) {                                                  // 1 ALU : 1 IMAD
+                if (i & 1) e[i] = __viaddmax_u16x2(e[i], xr, yr);
+                else e[i] = e[i] * xr + yr;
+            }
+            if constexpr (V == 17) {                                                  // 2 ALU : 1 IMAD
+                if (i % 3 != 2) e[i] = __viaddmax_u16x2(e[i], xr, yr);
+                else e[i] = e[i] * xr + yr;
+            }
+            if constexpr (V == 18) e[i] = __viaddmin_u16x2(e[i], xr, yr);             // VIADDMNMX.U16x2 min
         }
         if constexpr (V == 12) {
             // six chains per mask word: one R2P sets P1..P6
@@ -134,7 +146,7 @@ void run(const char *name, const char *pipe, unsigned *d, int sms, int ctas_per_
     for (int s = 0; s < sms; ++s) {
         if (!cnt[s]) continue;
         const double w = (double)(hi[s] - lo[s]);
-        rate += (double)cnt[s] * threads / 32 * iters * (V == 12 ? 48 : V >= 10 ? 32 : 8) / (4 * w);
+        rate += (double)cnt[s] * threads / 32 * iters * (V == 12 ? 48 : V == 10 || V == 11 ? 32 : 8) / (4 * w);
         win += w;
         ++used;
     }
@@ -176,5 +188,12 @@ int main()
     run<0>("VIADDMNMX.U16x2 4w/SMSP", "alu", d, sms, 1);
     run<12>("walk 6 chains per R2P", "mix", d, sms);
     run<12>("walk 6 chains, 4w/SMSP", "mix", d, sms, 1);
+    // round 2b: the job-pair heads' mix (FMA-pipe multiply-adds beside the ALU ops)
+    run<13>("IMAD", "fma", d, sms);
+    run<14>("PRMT", "alu?", d, sms);
+    run<15>("IMAD.HI", "fma", d, sms);
+    run<16>("VIADDMNMX|IMAD 1:1", "mix", d, sms);
+    run<17>("VIADDMNMX|IMAD 2:1", "mix", d, sms);
+    run<18>("VIADDMNMX.U16x2 (min)", "alu", d, sms);
     return 0;
 }
