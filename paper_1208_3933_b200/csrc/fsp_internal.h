@@ -32,6 +32,10 @@ struct __align__(8) fsp_rec {
 // half padded from ceil(maxm/2) to a multiple of 4 words.
 static inline int fsp_pq_words(int maxm) { return 2 * ((((maxm + 1) / 2) + 3) & ~3); }
 
+// u32 words per PTM row of the job-pair (jp) plans: 16-bit machine pairs
+// p_{j,2i} | p_{j,2i+1} << 16, padded to 16-byte rows.
+static inline int fsp_ptm16_words(int m) { return ((m + 1) / 2 + 3) & ~3; }
+
 // Dynamic shared-memory layout of the lb kernel (byte offsets).
 struct fsp_lb_layout {
     size_t off_u, u_bytes;     // U[(n+1)][urow_words] u32 transposed unscheduled sets (nibble

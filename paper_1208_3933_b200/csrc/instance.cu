@@ -95,14 +95,21 @@ static std::vector<int32_t> ptm_image(const int32_t *ptm, int n, int m, const fs
 {
     const int mp4 = (m + 3) & ~3;
     std::vector<int32_t> p32(pl.L.ptm_bytes / 4, 0);
-    for (int j = 0; j < n; ++j)
-        for (int k = 0; k < m; ++k) p32[(size_t)j * mp4 + k] = ptm[(size_t)j * m + k];
-    if (pl.jp) {
-        uint32_t *jp = reinterpret_cast<uint32_t *>(p32.data() + (size_t)n * mp4);
+    if (pl.jp) { // 16-bit machine-pair rows for the C pass, then the job-pair rows
+        const int w16 = fsp_ptm16_words(m);
+        uint32_t *p16 = reinterpret_cast<uint32_t *>(p32.data());
+        for (int j = 0; j < n; ++j)
+            for (int k = 0; k < m; ++k)
+                p16[(size_t)j * w16 + k / 2] |= (uint32_t)ptm[(size_t)j * m + k] << (16 * (k & 1));
+        uint32_t *jp = p16 + (size_t)n * w16;
         for (int j = 0; j < n; ++j)
             for (int k = 0; k < m; ++k)
                 jp[(size_t)(j / 2) * mp4 + k] |= (uint32_t)ptm[(size_t)j * m + k] << (16 * (j & 1));
-    } else if (pl.s16 && pl.maxm >= 10) { // nibble/TMEM variants: packed (p, q) machine pairs
+        return p32;
+    }
+    for (int j = 0; j < n; ++j)
+        for (int k = 0; k < m; ++k) p32[(size_t)j * mp4 + k] = ptm[(size_t)j * m + k];
+    if (pl.s16 && pl.maxm >= 10) { // nibble/TMEM variants: packed (p, q) machine pairs
         const int W = fsp_pq_words(pl.maxm), H = W / 2;
         uint32_t *pq = reinterpret_cast<uint32_t *>(p32.data() + (size_t)n * mp4);
         for (int j = 0; j < n; ++j) {

@@ -200,6 +200,8 @@ struct LbArgs {
     int lane_ingest;       // scheduled-set build with one node per lane (byte and
                            // lane-major rows); 0: the warp-per-node pass
     int jp;                // job-pair heads (fsp_lb_plan::jp): s_pq holds the job-pair rows
+                           // and the C pass reads 16-bit PTM pair rows
+    int prow;              // u32 words per PTM row in shared memory (mp4, or m/2 padded to 4)
     uint32_t jp_m;         // their masking offset M (multiple of 16)
     uint32_t one;          // 1 (a multiplier ptxas keeps on the FMA pipe)
     int dbg_skip;          // diagnostics only (FSP_LB_DEBUG_SKIP): bit 0 skips the
@@ -434,7 +436,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                    (ULayout<S16, NPL, MAXM, BYTE>::NIB ? (size_t)warp * (n + 1) * a.L.urow_words : 0);
     const int32_t *s_ptm = reinterpret_cast<const int32_t *>(smem + a.L.off_ptm);
     // TM variants: per job [p pairs x HMP][q pairs x HMP] u32 after PTM (see fsp_plan_lb)
-    const uint32_t *s_pq = reinterpret_cast<const uint32_t *>(s_ptm + (size_t)a.n * a.mp4);
+    // jp plans: PTM rows of packed 16-bit machine pairs (a.prow words), then the
+    // job-pair rows; else int32 rows (mp4 words), then the (p, q) pair rows
+    const uint32_t *s_pq = reinterpret_cast<const uint32_t *>(s_ptm + (size_t)a.n * a.prow);
     uint64_t *s_bar = reinterpret_cast<uint64_t *>(smem + a.L.off_bar);
     // per-warp heads R[MAXM][TN], A = R + L [MAXM][TN] (L_k = sum of p_jk over
     // the unscheduled jobs) and tails Q[MAXM][TN]; int16 in the s16 walk (all
@@ -779,6 +783,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 }
             }
             const uint32_t one = a.one;
+            // one job of the prefix: C_k = max(C_k, C'_k-1) + p_jk;
+            // max(C_k, C'_k-1) + p = max(C'_k-1 + p, C_k + p): the second sum on
+            // the FMA pipe (one * p + C), one VIADDMNMX on the ALU pipe
             auto step = [&](uint32_t job) {
                 if (job >= (uint32_t)n) {
                     bad = true;
@@ -795,12 +802,37 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                         for (int t = 0; t < 4; ++t) {
                             const int k = 4 * k4 + t;
                             if (k < MAXM && k < m) {
-                                // max(C_k, C'_k-1) + p = max(C'_k-1 + p, C_k + p):
-                                // the second sum on the FMA pipe (one * p + C),
-                                // one VIADDMNMX on the ALU pipe
                                 C[k] = __viaddmax_s32(prev, pv[t], pv[t] * (int)one + C[k]);
                                 prev = C[k];
                             }
+                        }
+                    }
+                }
+            };
+            // jp plans: 16-bit PTM rows (half the gathered bytes), word i =
+            // p_2i | p_2i+1 << 16; the chain runs in low halves (VIADDMNMX.U16x2,
+            // the high halves collect garbage, masked off after the pass), odd
+            // machines through a half swap
+            auto step16 = [&](uint32_t job) {
+                if (job >= (uint32_t)n) {
+                    bad = true;
+                    job = 0;
+                }
+                const uint4 *pr = reinterpret_cast<const uint4 *>(s_ptm + job * a.prow);
+                uint32_t prev = 0;
+#pragma unroll
+                for (int c4 = 0; c4 < (MAXM / 2 + 3) / 4; ++c4) {
+                    const uint4 v = pr[c4];
+                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int k = 2 * (4 * c4 + t);
+                        if (k + 1 < MAXM) {
+                            const uint32_t w = w4[t], ws = __byte_perm(w, w, 0x1032);
+                            prev = __viaddmax_u16x2(prev, w, w * one + (uint32_t)C[k]);
+                            C[k] = (int)prev;
+                            prev = __viaddmax_u16x2(prev, ws, ws * one + (uint32_t)C[k + 1]);
+                            C[k + 1] = (int)prev;
                         }
                     }
                 }
@@ -815,26 +847,33 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                     else atomicAnd(&Uw[job * urow + useg + q], ~lanebit);
                 }
             };
-            auto step_clr = [&](uint32_t job) {
-                clr(job);
-                step(job);
-            };
-            int i = 0;
-            // 16-byte rows: eight job ids per vector load; the eight clears
-            // follow the eight steps, so no shared store sits between a step's
-            // PTM-row loads and the previous step (the loads can be hoisted)
-            if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
-                const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
-                for (; i + 8 <= dd; i += 8) {
-                    const uint4 v = r4[i >> 3];
-                    const uint32_t w8[4] = {v.x, v.y, v.z, v.w};
+            // the prefix pass with step function ST (no branch between the jobs
+            // of a vector: the scheduler overlaps consecutive jobs' chains)
+            auto pass = [&](auto &&st) {
+                int i = 0;
+                // 16-byte rows: eight job ids per vector load; the eight clears
+                // follow the eight steps
+                if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+                    const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
+                    for (; i + 8 <= dd; i += 8) {
+                        const uint4 v = r4[i >> 3];
+                        const uint32_t w8[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) step(t & 1 ? w8[t >> 1] >> 16 : w8[t >> 1] & 0xffffu);
+                        for (int t = 0; t < 8; ++t) st(t & 1 ? w8[t >> 1] >> 16 : w8[t >> 1] & 0xffffu);
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) clr(t & 1 ? w8[t >> 1] >> 16 : w8[t >> 1] & 0xffffu);
+                        for (int t = 0; t < 8; ++t) clr(t & 1 ? w8[t >> 1] >> 16 : w8[t >> 1] & 0xffffu);
+                    }
                 }
-            }
-            for (; i < dd; ++i) step_clr(row[i]);
+                for (; i < dd; ++i) {
+                    const uint32_t job = row[i];
+                    clr(job);
+                    st(job);
+                }
+            };
+            bool j16 = false;
+            if constexpr (TM && !SPARSE && EXACT) j16 = a.jp != 0;
+            if (j16) pass(step16);
+            else pass(step);
             if (fused) __syncwarp(); // every lane's bits of node group q cleared
             // a2/a3: r_j0 = C_0, r_jk = max(C_k, r_j,k-1 + p_j,k-1) (R3); R_k =
             // min over unscheduled j (R5); Q_l = min_j q_jl, q_jl = sum_{i>l}
@@ -846,6 +885,8 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             if constexpr (TM && !SPARSE && EXACT) {
                 if (a.jp && (a.dbg_skip & 4)) continue; // diagnostics: C pass only
                 if (a.jp) { // rows a2/a3 by job pairs (jp_heads), then the TMEM stores
+#pragma unroll
+                    for (int k = 0; k < MAXM; ++k) C[k] &= 0xffff; // the 16-bit C pass's garbage
                     if (jp_heads<MAXM, HM, NPLP, UL>(a, s_pq, Uw, urow, useg, lane, q, C, tbase, n,
                                                      node < pool ? n - d : 0))
                         bad = true;
@@ -1429,9 +1470,8 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
             L.off_u = 0;
             // + the packed (p, q) machine-pair rows of the TM (nibble) variants
             // jp plans: + the job-pair rows [ceil(n/2)][mp4] (p_2i,k | p_2i+1,k << 16)
-            L.ptm_bytes = align16((size_t)n * mp4 * 4) +
-                          (pl.jp ? (size_t)((n + 1) / 2) * mp4 * 4
-                                 : nib ? (size_t)n * fsp_pq_words(pl.maxm) * 4 : 0);
+            L.ptm_bytes = pl.jp ? (size_t)n * fsp_ptm16_words(m) * 4 + (size_t)((n + 1) / 2) * mp4 * 4
+                                : align16((size_t)n * mp4 * 4) + (nib ? (size_t)n * fsp_pq_words(pl.maxm) * 4 : 0);
             L.off_ptm = L.u_bytes;
             L.off_bar = L.off_ptm + L.ptm_bytes;
             // nibble variants keep R/A/Q in TMEM: ceil(W/4) blocks of 3*ceil(maxm/2)*npl
@@ -1568,6 +1608,7 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.tables = tables;
     a.ptm = sparse ? inst->d_ptm32s_bb : inst->d_ptm32s;
     a.jp = pl.jp ? 1 : 0;
+    a.prow = pl.jp ? fsp_ptm16_words(inst->m) : (inst->m + 3) & ~3;
     a.jp_m = (uint32_t)pl.jp_m;
     a.one = 1u;
     a.cin = cin;
