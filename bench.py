@@ -471,12 +471,12 @@ def main():
                "d2h_bytes_per_step": int(a.pool * 4)}
 
     # the other BASELINE.json configs (driver-visible, same run, device-timed):
-    # 20x5, 20x20, 50x20 on 1M-node D1 pools, 500x20 on 262K
+    # 1M-node D1 pools (500x20 pools to 2^20)
     other = None
     if not a.no_configs and world == 1 and a.strong_total == 0:
         other = {}
         for cfg2, pool2 in (("ta001", 1 << 20), ("ta021", 1 << 20), ("ta051", 1 << 20),
-                            ("ta111", 1 << 18)):
+                            ("ta111", 1 << 20)):
             if cfg2 == cfg:
                 continue
             n2, m2, seed2 = inputs.TAILLARD_SEEDS[cfg2]

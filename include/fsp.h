@@ -96,6 +96,9 @@ typedef struct {
     int32_t smem_bytes;
     int32_t tail_split;       /* split of the last, partial tile iteration    */
     int32_t heads_jp;         /* 1: heads/tails/loads by job pairs (16x2 ops) */
+    int32_t mapping;          /* 0: nodes over lanes (4 per lane); 1: warp per
+                                 node, lanes over couples (A/B, FSP_LB_MAPPING=warp
+                                 at fsp_instance_load)                         */
 } fsp_lb_launch;
 
 int fsp_lb_launch_info(const fsp_instance *inst, int64_t pool, int32_t sibling,

@@ -51,7 +51,7 @@ class LaunchInfo(C.Structure):
     _fields_ = [(f, C.c_int32) for f in (
         "grid", "warps_per_cta", "split", "iterations", "groups", "pairs_per_group",
         "group_buffers", "nodes_per_lane", "row_layout", "tmem_cols", "sparse_walk",
-        "smem_bytes", "tail_split", "heads_jp")]
+        "smem_bytes", "tail_split", "heads_jp", "mapping")]
 
 
 class BBStats(C.Structure):

@@ -101,6 +101,10 @@ struct fsp_instance {
     uint8_t *d_tables_bb; // tables laid out for plan_bb
     fsp_fam_layout fam;   // family kernel tables (n <= 256)
     uint8_t *d_fam;
+    // A/B (FSP_LB_MAPPING=warp at load): dense pools bounded by the warp-per-
+    // sub-problem kernel of wpn.cu, records [groups][n][32] int2
+    bool wpn;
+    void *d_wpn;
     // host-API staging (lazily created, guarded by a mutex in api.cu)
     void *host_ctx;
 };
@@ -116,6 +120,11 @@ int fsp_launch_family(const fsp_instance *inst, const uint16_t *ppf, int32_t str
 // buffer size (hybrid.cu runs several on one device)
 int fsp_bb_init_ex(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_t world,
                    double mem_frac, int64_t children_cap, bool root_only, void **state);
+
+// warp-per-sub-problem A/B kernel (wpn.cu)
+int fsp_wpn_build(fsp_instance *inst);
+int fsp_launch_lb_wpn(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
+                      const int32_t *depth, int64_t pool, int32_t *lb_out, cudaStream_t s);
 
 // thread-local last error
 int fsp_fail(int code, const std::string &msg);

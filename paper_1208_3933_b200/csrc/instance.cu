@@ -16,6 +16,7 @@
 #include <cstring>
 #include <new>
 #include <numeric>
+#include <string>
 #include <vector>
 
 #include "fsp_internal.h"
@@ -196,6 +197,8 @@ extern "C" int fsp_instance_load(const int32_t *ptm, int32_t n, int32_t m, fsp_i
         return fsp_cuda_fail(e, "instance upload");
     }
     rc = fsp_fam_build(inst);
+    if (rc == FSP_OK && getenv("FSP_LB_MAPPING") && std::string(getenv("FSP_LB_MAPPING")) == "warp")
+        rc = fsp_wpn_build(inst);
     if (rc != FSP_OK) {
         fsp_instance_free(inst);
         return rc;
@@ -217,6 +220,7 @@ extern "C" void fsp_instance_free(fsp_instance *inst)
     if (inst->d_ptm32) cudaFree(inst->d_ptm32);
     if (inst->d_err) cudaFree(inst->d_err);
     if (inst->d_fam) cudaFree(inst->d_fam);
+    if (inst->d_wpn) cudaFree(inst->d_wpn);
     delete[] inst->h_ptm;
     delete inst;
 }
@@ -265,5 +269,6 @@ extern "C" int fsp_lb_launch_info(const fsp_instance *inst, int64_t pool, int32_
     out->smem_bytes = (int32_t)pl.smem_bytes;
     out->tail_split = sibling ? 1 : fsp_lb_tail_split(pl, pool, split);
     out->heads_jp = pl.jp ? 1 : 0;
+    out->mapping = !sibling && inst->wpn ? 1 : 0;
     return FSP_OK;
 }

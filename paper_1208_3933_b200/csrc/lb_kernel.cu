@@ -1435,7 +1435,7 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
     // smaller live sets no longer outweigh the per-node table and mask traffic)
     if (pl.sparse) npl_lo = npl_hi = getenv("FSP_BB_NPL") && atoi(getenv("FSP_BB_NPL")) == 2 ? 2 : 4;
     int w_lo = 1, w_hi = pl.maxm > 20 ? 8 : pl.maxm <= 5 ? 4 : 16; // = the kernel's launch bounds
-    if (const char *s = getenv("FSP_LB_WARPS")) w_lo = w_hi = std::max(1, std::min(w_hi, atoi(s)));
+    if (const char *s = getenv(sparse ? "FSP_BB_WARPS" : "FSP_LB_WARPS")) w_lo = w_hi = std::max(1, std::min(w_hi, atoi(s)));
     double best = -1.0;
     fsp_lb_plan bestp = pl;
     for (int npl = npl_lo; npl <= npl_hi; npl += 2) {
@@ -1522,9 +1522,11 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                     // allocation beyond them would wait for another CTA to exit)
                     if (occupancy_of(c) == FSP_OK && c.ctas_per_sm > 0 &&
                         c.ctas_per_sm * tm_cols <= 512) {
-                        // byte rows: one FMA op less per position (+11 % at 200x20)
+                        // byte rows: one FMA op less per position and the fused
+                        // lane ingest (+11 % at 200x20; 500x20: 8 warps of byte
+                        // rows 14.6 ms vs 12 warps of nibble rows 15.3 ms)
                         const double score = (double)W * c.ctas_per_sm * (npl == 4 ? 1.5 : 1.0) *
-                                             (nib && lay == 0 ? 1.1 : 1.0) /
+                                             (nib && lay == 0 ? 1.25 : 1.0) /
                                              (1.0 + (db ? 0.005 : 0.015) * (Greal - 1));
                         if (score > best) {
                             best = score;
@@ -1591,6 +1593,7 @@ int fsp_lb_tail_split(const fsp_lb_plan &pl, int64_t pool, int split)
 int fsp_launch_lb(const fsp_instance *inst, const uint16_t *prefix, int32_t stride,
                   const int32_t *depth, int64_t pool, int32_t *lb_out, cudaStream_t s)
 {
+    if (inst->wpn) return fsp_launch_lb_wpn(inst, prefix, stride, depth, pool, lb_out, s);
     return fsp_launch_lb_dev(inst, prefix, stride, depth, pool, nullptr, nullptr, 0, false, lb_out, s,
                              0);
 }

@@ -306,18 +306,24 @@ def _sampled(torch, fsp, orc, ptm, pf, dp, k, seed):
     return inst, got
 
 
-def test_full_size_500x20_bench_shape(torch, fsp, orc):
-    """BASELINE configs[4] (ta111-class 500x20) at a 262,144-node D1 pool plus a
-    ragged tail of 77 nodes: the launch shape is the bench one (no couple
-    split, several tile iterations per CTA, every couple group cycling through
-    the TMA buffers), checked on 3,000 random nodes and the last 200."""
+@pytest.mark.parametrize("rows", ["planner", "nibble"])
+def test_full_size_500x20_bench_shape(torch, fsp, orc, monkeypatch, rows):
+    """BASELINE configs[4] (ta111-class 500x20) at the bench's 1,048,576-node D1
+    pool plus a ragged tail of 77 nodes: the launch shape is the bench one (no
+    couple split, several tile iterations per CTA, every couple group cycling
+    through the TMA buffers; the planner's byte rows with 8 warps, and the
+    12-warp nibble rows of FSP_LB_ROWS=1), checked on 3,000 random nodes and
+    the last 200."""
+    if rows == "nibble":
+        monkeypatch.setenv("FSP_LB_ROWS", "1")
     n, m, seed = inputs.TAILLARD_SEEDS["ta111"]
     ptm = inputs.taillard(n, m, seed)
-    N = (1 << 18) + 77
+    N = (1 << 20) + 77
     pf, dp = inputs.pool_d1(n, N, inputs.pool_seed("ta111"))
     inst = fsp.Instance(ptm)
     li = inst.launch_info(N)
     assert li["split"] == 1 and li["iterations"] > 1 and li["groups"] > li["group_buffers"]
+    assert li["row_layout"] == (2 if rows == "nibble" else 1) and li["heads_jp"] == 1
     _, got = _sampled(torch, fsp, orc, ptm, pf, dp, 3000, 11)
     assert got.min() >= int(ptm.sum(0).max()) and got.max() <= (n + m - 1) * int(ptm.max())
 
@@ -474,3 +480,37 @@ def test_parity_records_in_global_memory(torch, fsp, orc, monkeypatch, name, N):
     assert (got == ref).all()
     sample = np.random.default_rng(3).choice(N, 500, replace=False)
     assert (got[sample] == orc.Tables(ptm).lb_eval(pf[sample], dp[sample])).all()
+
+
+# ------------------------------ A/B: the north_star's warp-per-sub-problem mapping
+
+@pytest.mark.parametrize("name,N", [("ta001", 5003), ("ta021", 4133), ("ta051", 2001), ("ta091", 1037)])
+def test_parity_warp_per_node_mapping(torch, fsp, orc, monkeypatch, name, N):
+    """FSP_LB_MAPPING=warp (wpn.cu: one warp per sub-problem, lanes over
+    couples, heads/tails by warp reductions) bounds the same pools bit for bit;
+    ragged batch tails and d = 0 / n - 1 / n nodes included."""
+    monkeypatch.setenv("FSP_LB_MAPPING", "warp")
+    n, m, seed = inputs.TAILLARD_SEEDS[name]
+    ptm = inputs.taillard(n, m, seed)
+    parts = [inputs.pool_d1(n, N, inputs.pool_seed(name) + 9),
+             inputs.pool_fixed_depth(n, 33, n, 91), inputs.pool_fixed_depth(n, 35, n - 1, 92),
+             inputs.pool_fixed_depth(n, 31, 0, 93)]
+    pf = np.concatenate([p[0] for p in parts])
+    dp = np.concatenate([p[1] for p in parts])
+    inst = compare(torch, fsp, orc, ptm, pf, dp)
+    assert inst.launch_info(len(dp))["mapping"] == 1
+
+
+def test_warp_per_node_mapping_flags_malformed(torch, fsp, monkeypatch):
+    """The A/B kernel raises the same malformed-node flag (job >= n, repeated job)."""
+    monkeypatch.setenv("FSP_LB_MAPPING", "warp")
+    n, m, seed = inputs.TAILLARD_SEEDS["ta021"]
+    inst = fsp.Instance(inputs.taillard(n, m, seed))
+    pf, dp = inputs.pool_fixed_depth(n, 64, 5, 7)
+    pf[3, 1] = pf[3, 0]  # repeated job
+    gpu_lb(torch, inst, pf, dp)
+    assert inst.check() == fsp.FSP_EBADNODE
+    pf, dp = inputs.pool_fixed_depth(n, 64, 5, 7)
+    pf[9, 2] = n + 3  # job out of range
+    gpu_lb(torch, inst, pf, dp)
+    assert inst.check() == fsp.FSP_EBADNODE

@@ -1,1 +1,1 @@
-for cfg in "" "FSP_LB_NPL=2" "FSP_LB_NPL=2 FSP_LB_WARPS=12" "FSP_LB_NPL=2 FSP_LB_WARPS=16" "FSP_LB_DBUF=1" "FSP_LB_ROWS=0" "FSP_LB_WARPS=4"; do echo "cfg: $cfg"; env $cfg timeout 120 python tools/lb_prof.py ta111:262144 2>&1 | cut -c1-400; done
+for w in 12 8; do for b in 2 3 4; do echo "WARPS=$w DBUF=$b"; FSP_LB_WARPS=$w FSP_LB_DBUF=$b timeout 300 python tools/lb_prof.py ta111:1048576; done; done > gpurun_out/sweep500.txt 2>&1
