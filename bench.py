@@ -466,8 +466,14 @@ def main():
         dt = float(tt.item())
         if not torch.equal(h_lb, d_lb.cpu()):
             raise SystemExit("host-API LBs differ from device LBs")
+        # bytes that cross PCIe per step: the zero-copy gather (pinned buffers)
+        # reads each node's depth and its first ceil(d/8) 16-byte vectors of
+        # prefix, not the row padding (api.cu gather_rows_kernel)
+        gathered = int(((np.minimum(dp, stride).astype(np.int64) + 7) // 8 * 16).sum()) + int(dp.nbytes)
         e2e = {"value": total_nodes * a.steps / dt, "unit": UNIT,
-               "h2d_bytes_per_step": int(pf.nbytes + dp.nbytes),
+               "h2d_bytes_per_step": gathered,
+               "h2d_note": "zero-copy gather of each node's depth and 2*depth prefix bytes "
+                           f"(the pinned pool is {int(pf.nbytes + dp.nbytes)} bytes with row padding)",
                "d2h_bytes_per_step": int(a.pool * 4)}
 
     # the other BASELINE.json configs (driver-visible, same run, device-timed):
