@@ -339,10 +339,12 @@ __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1
 // Per pair: 2 x m - 1 ALU ops for the heads, m - 1 for the tails, ~4 for the
 // flags; the loads' and the tails' running sums are FMA-pipe multiply-adds.
 // Returns true for a malformed node (unscheduled count != n - depth).
-template <int MAXM, int HM, int NPLP, class UL>
+// TM: R/A/Q to tensor memory as machine pairs (column (arr*HM + k/2)*NPLP + q);
+// else to the warp's shared arrays Rs/As/Qs [MAXM][TN] (16-bit), node q*32+lane.
+template <int MAXM, int HM, int NPLP, class UL, bool TM, int TN>
 __device__ __forceinline__ bool jp_heads(const LbArgs &a, const uint32_t *s_jp, const uint32_t *Uw,
                                          int urow, int useg, int lane, int q, const int (&C)[MAXM],
-                                         uint32_t tbase, int n, int want)
+                                         uint32_t tbase, uint16_t *Rs, int n, int want)
 {
     constexpr int MP4 = (MAXM + 3) & ~3;
     uint32_t C2[MAXM], RR[MAXM], QQ[MAXM], LL[MAXM];
@@ -391,26 +393,40 @@ __device__ __forceinline__ bool jp_heads(const LbArgs &a, const uint32_t *s_jp, 
         for (int k = 0; k < MAXM; ++k) LL[k] = pw[k] * absw + LL[k];
     }
     const int cnt = (int)((cnt2 & 0xffffu) + (cnt2 >> 16));
-    uint32_t R2[HM], A2[HM], Q2[HM];
+    if constexpr (!TM) {
+        uint16_t *As = Rs + MAXM * TN, *Qs = As + MAXM * TN;
 #pragma unroll
-    for (int kp = 0; kp < HM; ++kp) {
-        const uint32_t r0 = RR[2 * kp], r1 = RR[2 * kp + 1];
-        const uint32_t q0 = QQ[2 * kp], q1 = 2 * kp + 1 == MAXM - 1 ? 0u : QQ[2 * kp + 1];
-        R2[kp] = __vminu2(__byte_perm(r0, r1, 0x5410), __byte_perm(r0, r1, 0x7632));
-        Q2[kp] = __vminu2(__byte_perm(q0, q1, 0x5410), __byte_perm(q0, q1, 0x7632));
-        A2[kp] = R2[kp] + __byte_perm(LL[2 * kp], LL[2 * kp + 1], 0x7632); // A = R + L
-        if (cnt == 0) { // R6: complete schedule, R = C, A = C, Q = 0
-            R2[kp] = A2[kp] = __byte_perm(C2[2 * kp], C2[2 * kp + 1], 0x5410);
-            Q2[kp] = 0u;
+        for (int k = 0; k < MAXM; ++k) {
+            const uint32_t r = __vminu2(RR[k], __byte_perm(RR[k], 0u, 0x1032));
+            const uint32_t qv = k == MAXM - 1 ? 0u : __vminu2(QQ[k], __byte_perm(QQ[k], 0u, 0x1032));
+            const uint32_t R = cnt ? (r & 0xffffu) : (C2[k] & 0xffffu); // R6: R = A = C, Q = 0
+            Rs[k * TN + q * 32 + lane] = (uint16_t)R;
+            As[k * TN + q * 32 + lane] = (uint16_t)(cnt ? R + (LL[k] >> 16) : R);
+            Qs[k * TN + q * 32 + lane] = (uint16_t)(cnt ? qv & 0xffffu : 0u);
         }
-    }
+        return cnt != want;
+    } else {
+        uint32_t R2[HM], A2[HM], Q2[HM];
 #pragma unroll
-    for (int kp = 0; kp < HM; ++kp) {
-        tm_st1(tbase + (0 * HM + kp) * NPLP + q, R2[kp]);
-        tm_st1(tbase + (1 * HM + kp) * NPLP + q, A2[kp]);
-        tm_st1(tbase + (2 * HM + kp) * NPLP + q, Q2[kp]);
+        for (int kp = 0; kp < HM; ++kp) {
+            const uint32_t r0 = RR[2 * kp], r1 = RR[2 * kp + 1];
+            const uint32_t q0 = QQ[2 * kp], q1 = 2 * kp + 1 == MAXM - 1 ? 0u : QQ[2 * kp + 1];
+            R2[kp] = __vminu2(__byte_perm(r0, r1, 0x5410), __byte_perm(r0, r1, 0x7632));
+            Q2[kp] = __vminu2(__byte_perm(q0, q1, 0x5410), __byte_perm(q0, q1, 0x7632));
+            A2[kp] = R2[kp] + __byte_perm(LL[2 * kp], LL[2 * kp + 1], 0x7632); // A = R + L
+            if (cnt == 0) { // R6: complete schedule, R = C, A = C, Q = 0
+                R2[kp] = A2[kp] = __byte_perm(C2[2 * kp], C2[2 * kp + 1], 0x5410);
+                Q2[kp] = 0u;
+            }
+        }
+#pragma unroll
+        for (int kp = 0; kp < HM; ++kp) {
+            tm_st1(tbase + (0 * HM + kp) * NPLP + q, R2[kp]);
+            tm_st1(tbase + (1 * HM + kp) * NPLP + q, A2[kp]);
+            tm_st1(tbase + (2 * HM + kp) * NPLP + q, Q2[kp]);
+        }
+        return cnt != want;
     }
-    return cnt != want;
 }
 
 // launch bounds: 8 warps for m > 20; 4 warps x 5 CTAs per SM for m = 5 (the
@@ -827,12 +843,14 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         const int k = 2 * (4 * c4 + t);
-                        if (k + 1 < MAXM) {
+                        if (k < MAXM) {
                             const uint32_t w = w4[t], ws = __byte_perm(w, w, 0x1032);
                             prev = __viaddmax_u16x2(prev, w, w * one + (uint32_t)C[k]);
                             C[k] = (int)prev;
-                            prev = __viaddmax_u16x2(prev, ws, ws * one + (uint32_t)C[k + 1]);
-                            C[k + 1] = (int)prev;
+                            if (k + 1 < MAXM) { // (odd m: the last machine has no pair)
+                                prev = __viaddmax_u16x2(prev, ws, ws * one + (uint32_t)C[k + 1]);
+                                C[k + 1] = (int)prev;
+                            }
                         }
                     }
                 }
@@ -871,7 +889,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 }
             };
             bool j16 = false;
-            if constexpr (TM && !SPARSE && EXACT) j16 = a.jp != 0;
+            if constexpr (!SPARSE && EXACT && S16) j16 = a.jp != 0;
             if (j16) pass(step16);
             else pass(step);
             if (fused) __syncwarp(); // every lane's bits of node group q cleared
@@ -882,13 +900,14 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             // are < 2^15, host-checked): tails q_jl come from a per-job table of
             // machine pairs (one VIMNMX.U16x2 per pair) and p_jl from another
             // (one add per pair), next to PTM in shared memory
-            if constexpr (TM && !SPARSE && EXACT) {
+            if constexpr (!SPARSE && EXACT && S16) {
                 if (a.jp && (a.dbg_skip & 4)) continue; // diagnostics: C pass only
                 if (a.jp) { // rows a2/a3 by job pairs (jp_heads), then the TMEM stores
 #pragma unroll
                     for (int k = 0; k < MAXM; ++k) C[k] &= 0xffff; // the 16-bit C pass's garbage
-                    if (jp_heads<MAXM, HM, NPLP, UL>(a, s_pq, Uw, urow, useg, lane, q, C, tbase, n,
-                                                     node < pool ? n - d : 0))
+                    if (jp_heads<MAXM, HM, NPLP, UL, TM, TN>(a, s_pq, Uw, urow, useg, lane, q, C, tbase,
+                                                             reinterpret_cast<uint16_t *>(Rs), n,
+                                                             node < pool ? n - d : 0))
                         bad = true;
                     continue;
                 }
@@ -1419,7 +1438,7 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
         }
         const int64_t M = (65535 - maxsum) & ~int64_t(15);
         pl.jp_m = (int)std::max<int64_t>(M, 0);
-        pl.jp = !sparse && pl.exact && pl.s16 && m >= 10 && M > (int64_t)(n + m) * inst->max_p &&
+        pl.jp = !sparse && pl.exact && pl.s16 && M > (int64_t)(n + m) * inst->max_p &&
                 (int64_t)((n + 1) / 2) * inst->max_p <= 65535;
         if (const char *s = getenv("FSP_LB_JP")) pl.jp = pl.jp && atoi(s) != 0;
     }

@@ -254,7 +254,7 @@ def test_parity_walk16_offset_boundary(torch, fsp, orc, n, m):
         assert inst.info["walk16"] == walk16
 
 
-@pytest.mark.parametrize("n,m", [(20, 20), (41, 10), (200, 20)])
+@pytest.mark.parametrize("n,m", [(20, 20), (41, 10), (200, 20), (20, 5), (33, 5)])
 def test_parity_heads_job_pairs_boundary(torch, fsp, orc, n, m):
     """Job-pair heads (lb_kernel.cu jp_heads) push a scheduled job's half to an
     offset M = (65535 - max_j sum_k p_jk) rounded down to 16 and are taken iff
@@ -277,7 +277,7 @@ def test_parity_heads_job_pairs_boundary(torch, fsp, orc, n, m):
         assert inst.launch_info(len(dp))["heads_jp"] == jp
 
 
-@pytest.mark.parametrize("name", ["ta021", "ta091"])
+@pytest.mark.parametrize("name", ["ta001", "ta021", "ta091"])
 def test_heads_job_pairs_ab(torch, fsp, orc, monkeypatch, name):
     """The same pool through the job-pair heads and the per-job heads
     (FSP_LB_JP=0, the A/B switch) gives identical LBs, equal to the oracle's."""
