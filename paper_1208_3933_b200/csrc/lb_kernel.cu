@@ -199,6 +199,7 @@ struct LbArgs {
                            // lane SETS its node's bits (deep nodes: n' << d entries)
     int lane_ingest;       // scheduled-set build with one node per lane (byte and
                            // lane-major rows); 0: the warp-per-node pass
+    int sort_depth;        // fused dense path: the tile's nodes ranked by depth over the slots
     int jp;                // job-pair heads (fsp_lb_plan::jp): s_pq holds the job-pair rows
                            // and the C pass reads 16-bit PTM pair rows
     int prow;              // u32 words per PTM row in shared memory (mp4, or m/2 padded to 4)
@@ -339,6 +340,41 @@ __device__ __forceinline__ void upd(uint32_t bits, uint32_t lanebit, uint32_t c1
 // Per pair: 2 x m - 1 ALU ops for the heads, m - 1 for the tails, ~4 for the
 // flags; the loads' and the tails' running sums are FMA-pipe multiply-adds.
 // Returns true for a malformed node (unscheduled count != n - depth).
+// Bitonic sort of the warp's 32*NPL keys, key q of lane L at position q*32+L
+// (in-lane stages exchange registers, cross-lane stages shfl.xor), ascending.
+template <int NPL>
+__device__ __forceinline__ void warp_sort(uint32_t (&e)[NPL], int lane)
+{
+    constexpr int N = 32 * NPL;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jq = j >> 5;
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) {
+                    if ((q & jq) == 0) {
+                        const int q2 = q | jq;
+                        const bool asc = (((q * 32 + lane) & k) == 0);
+                        const uint32_t lo = min(e[q], e[q2]), hi = max(e[q], e[q2]);
+                        e[q] = asc ? lo : hi;
+                        e[q2] = asc ? hi : lo;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) {
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, e[q], j);
+                    const bool asc = (((q * 32 + lane) & k) == 0);
+                    const bool keep_min = ((lane & j) == 0) == asc;
+                    e[q] = keep_min ? min(e[q], o) : max(e[q], o);
+                }
+            }
+        }
+    }
+}
+
 // TM: R/A/Q to tensor memory as machine pairs (column (arr*HM + k/2)*NPLP + q);
 // else to the warp's shared arrays Rs/As/Qs [MAXM][TN] (16-bit), node q*32+lane.
 template <int MAXM, int HM, int NPLP, class UL, bool TM, int TN>
@@ -580,8 +616,13 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
         bool bad = false;
 
         // ---------------- a1: node ingest (depth, scheduled set) ----------------
-        // lane `lane` owns nodes tile*TN + q*32 + lane, q < NPL
+        // slot (q, lane) holds node tile*TN + sidx[q]: q*32 + lane, or, with the
+        // fused C pass (a.sort_depth), the tile's nodes ranked by depth, so the
+        // 32 prefixes a C-pass step walks together are about equally long (the
+        // pass runs to the deepest of them)
+        const bool fused = !SPARSE && !a.cin && a.lane_ingest && (!UL::NIB || UL::BYTES);
         int dq[NPL];
+        uint32_t sidx[NPL];
         uint32_t validq[NPL];
         uint32_t anyvalid = 0;
 #pragma unroll
@@ -594,7 +635,22 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 d = 0;
             }
             dq[q] = d;
-            validq[q] = __ballot_sync(0xffffffffu, has);
+            sidx[q] = (uint32_t)(q * 32 + lane);
+        }
+        if (fused && a.sort_depth) {
+            uint32_t key[NPL];
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) key[q] = ((uint32_t)dq[q] << 8) | sidx[q];
+            warp_sort<NPL>(key, lane);
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                dq[q] = (int)(key[q] >> 8);
+                sidx[q] = key[q] & 0xffu;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            validq[q] = __ballot_sync(0xffffffffu, tile * TN + sidx[q] < pool);
             anyvalid |= validq[q];
         }
         // all-unscheduled pattern of this warp's segment
@@ -618,8 +674,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
         __syncwarp();
         // dense pools whose prefix completion times are computed here (no cin):
         // each lane clears its node's bits in the same pass over the prefix
-        // that computes C (phase A below), reading every prefix once
-        const bool fused = !SPARSE && !a.cin && a.lane_ingest && (!UL::NIB || UL::BYTES);
+        // that computes C (phase A below), reading every prefix once (fused)
         if (fused) {
             // (scheduled bits cleared in phase A)
         } else if (a.lane_ingest && !UL::NIB || a.lane_ingest && UL::BYTES) {
@@ -767,11 +822,15 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
         // ---------------- per node of this lane: C, heads, tails ----------------
 #pragma unroll 1
         for (int q = 0; q < ((a.dbg_skip & 1) ? 0 : NPL); ++q) {
-            const long long node = tile * TN + q * 32 + lane;
             int d = dq[0]; // (select chain: no local-memory indexing)
+            uint32_t si = sidx[0];
 #pragma unroll
             for (int t = 1; t < NPL; ++t)
-                if (q == t) d = dq[t];
+                if (q == t) {
+                    d = dq[t];
+                    si = sidx[t];
+                }
+            const long long node = tile * TN + si;
             // prefix completion times C_k
             int C[MAXM];
 #pragma unroll
@@ -1280,7 +1339,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
         }
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
-            const long long node = tile * TN + q * 32 + lane;
+            const long long node = tile * TN + sidx[q];
             if (node < pool) {
                 if (split == 1) a.lb_out[node] = lb[q];
                 else atomicMax(&a.lb_out[node], lb[q]);
@@ -1630,6 +1689,7 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.tables = tables;
     a.ptm = sparse ? inst->d_ptm32s_bb : inst->d_ptm32s;
     a.jp = pl.jp ? 1 : 0;
+    a.sort_depth = getenv("FSP_LB_SORT") ? atoi(getenv("FSP_LB_SORT")) : 1;
     a.prow = pl.jp ? fsp_ptm16_words(inst->m) : (inst->m + 3) & ~3;
     a.jp_m = (uint32_t)pl.jp_m;
     a.one = 1u;
