@@ -319,17 +319,32 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
                 nc += __popc(bal);
             }
             __syncwarp();
+            const bool v4 = (m & 3) == 0 && (reinterpret_cast<uintptr_t>(ptm) & 15) == 0;
             for (int i = lane; i < nc; i += 32) {
                 const int j = (int)keys[i];
                 long long idle = 0;
                 int prev = 0;
                 const int32_t *pj = ptm + (size_t)j * m;
+                if (v4 && by_idle) { // 16-byte PTM loads (m % 4 == 0)
+                    for (int k = 0; k < m; k += 4) {
+                        const int4 pv = __ldg(reinterpret_cast<const int4 *>(pj + k));
+                        const int pk[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const int ck = cs[k + t];
+                            const int start = max(ck, prev);
+                            idle += start - ck;
+                            prev = start + pk[t];
+                        }
+                    }
+                } else {
 #pragma unroll 4
-                for (int k = 0; k < (by_idle ? m : 0); ++k) { // (by_idle = 0: job order, A/B only)
-                    const int ck = cs[k];
-                    const int start = max(ck, prev);
-                    idle += start - ck;
-                    prev = start + __ldg(pj + k);
+                    for (int k = 0; k < (by_idle ? m : 0); ++k) { // (by_idle = 0: job order, A/B only)
+                        const int ck = cs[k];
+                        const int start = max(ck, prev);
+                        idle += start - ck;
+                        prev = start + __ldg(pj + k);
+                    }
                 }
                 keys[i] = ((unsigned long long)idle << 12) | (unsigned)j;
             }
@@ -338,7 +353,31 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
             // (= key ranks cur .. cur+g-1), one warp-min round per child
             long long thr = st.kl[src];
             unsigned long long mykey = 0ull;
-            for (int t = 0; t < g; ++t) {
+            // at most 32 candidates whose keys fit 32 bits (deep parents, the
+            // bulk of the search): one bitonic sort of the warp's keys, then
+            // the g keys after the ones already taken (<= thr) by shuffles
+            bool sorted = false;
+            if (nc <= 32) {
+                const unsigned long long kk = lane < nc ? keys[lane] : 0ull;
+                if (__all_sync(0xffffffffu, kk < 0xffffffffull)) {
+                    uint32_t k32 = lane < nc ? (uint32_t)kk : 0xffffffffu;
+#pragma unroll
+                    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+                        for (int j = k >> 1; j > 0; j >>= 1) {
+                            const uint32_t o = __shfl_xor_sync(0xffffffffu, k32, j);
+                            const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+                            k32 = keep_min ? min(k32, o) : max(k32, o);
+                        }
+                    }
+                    const int pos = __popc(__ballot_sync(0xffffffffu, lane < nc && (long long)k32 <= thr));
+                    const uint32_t mine = __shfl_sync(0xffffffffu, k32, (pos + lane) & 31);
+                    if (lane < g) mykey = mine;
+                    if (g > 0) thr = (long long)__shfl_sync(0xffffffffu, k32, (pos + g - 1) & 31);
+                    sorted = true;
+                }
+            }
+            for (int t = 0; t < (sorted ? 0 : g); ++t) {
                 unsigned long long best = ~0ull;
                 for (int i = lane; i < nc; i += 32) {
                     const unsigned long long k = keys[i];
@@ -393,14 +432,26 @@ __global__ void expand_kernel(Nodes st, int64_t first, int64_t B, const int64_t 
             // C'_k = max(C'_k-1, C_k) + p_jk, a serial max-plus pass over the
             // machines per lane (all g children at once)
             if (lane < g) {
-                const int32_t *pc = st.C + (size_t)src * m;
                 const int32_t *pj = ptm + (size_t)myj * m;
                 int32_t *cc = ch.C + (size_t)(c0 + lane) * m;
                 int prev = 0;
+                if ((m & 3) == 0 && ((reinterpret_cast<uintptr_t>(cc) | reinterpret_cast<uintptr_t>(pj)) & 15) == 0) {
+                    // 16-byte loads and stores; the parent's C from shared memory
+                    for (int k = 0; k < m; k += 4) {
+                        const int4 pv = __ldg(reinterpret_cast<const int4 *>(pj + k));
+                        int4 o;
+                        o.x = prev = max(prev, cs[k]) + pv.x;
+                        o.y = prev = max(prev, cs[k + 1]) + pv.y;
+                        o.z = prev = max(prev, cs[k + 2]) + pv.z;
+                        o.w = prev = max(prev, cs[k + 3]) + pv.w;
+                        *reinterpret_cast<int4 *>(cc + k) = o;
+                    }
+                } else {
 #pragma unroll 4
-                for (int k = 0; k < m; ++k) {
-                    prev = max(prev, pc[k]) + pj[k];
-                    cc[k] = prev;
+                    for (int k = 0; k < m; ++k) {
+                        prev = max(prev, cs[k]) + pj[k];
+                        cc[k] = prev;
+                    }
                 }
                 ch.dp[c0 + lane] = d + 1;
                 ch_key[c0 + lane] = mykey;
