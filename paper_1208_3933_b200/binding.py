@@ -13,7 +13,10 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfsp.so")
+# (FSP_LIB_VARIANT: diagnostics, a compile-time A/B build of the same library
+# under paper_1208_3933_b200/_build/variants/, tools/build_variant.py)
+LIB_PATH = os.path.join(_HERE, "libfsp.so") if not os.environ.get("FSP_LIB_VARIANT") else \
+    os.path.join(_HERE, "_build", "variants", f"libfsp_{os.environ['FSP_LIB_VARIANT']}.so")
 
 FSP_OK, FSP_EINVAL, FSP_ERANGE, FSP_ENOMEM, FSP_ECUDA = 0, -1, -2, -3, -4
 FSP_ENOTFOUND, FSP_EBUDGET, FSP_EBADNODE = -5, -6, -7

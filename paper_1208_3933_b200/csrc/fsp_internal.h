@@ -66,6 +66,7 @@ struct fsp_lb_plan {
     bool jp;             // dense TM plans: job-pair heads (PTM + job-pair rows staged, no pq
                          //   rows; lb_kernel.cu jp_heads), jp_m = the masking offset M
     int jp_m;
+    bool kcache;         // dense 20-machine walks: R_k, A_k cached while k is unchanged (n <= 64)
     bool recs_global;    // ablation: couple records read from global memory (20-machine dense)
     int warps;           // warps per CTA
     int ctas_per_sm;

@@ -31,6 +31,7 @@
 
 #include "fsp_internal.h"
 
+
 namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -470,7 +471,10 @@ __device__ __forceinline__ bool jp_heads(const LbArgs &a, const uint32_t *s_jp, 
 // fit; measured 20x5: 5.0 G bounds/s vs 3.9 G with one 16-warp CTA); else 16
 // RG (placement ablation, NEXT-3): the couple records are read from global
 // memory (L1/L2, read-only path) instead of the TMA-staged shared buffers.
-template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE, bool BYTE = true, bool RG = false>
+// KC (dense TMEM walks, short job lists: fsp_lb_plan::kcache): R_k and A_k are
+// kept in registers while k is unchanged, as in the sparse walk (20x20 +5 %;
+// at 200x20 the extra live registers cost 0.7 %, profiles/r02/dense_kcache_ab.txt)
+template <int MAXM, bool EXACT, bool S16, int NPL, bool SPARSE, bool BYTE = true, bool RG = false, bool KC = false>
 __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM <= 5 ? 5 : 1)
     lb_kernel(const LbArgs a)
 {
@@ -1160,7 +1164,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 // lines 06-07: timeOnM1 / timeOnM2 start at the RM minima, so
                 // e = t2 - t1 starts at R_l - R_k (>= 0)
                 int ee[NPL], fin[NPL]; // SPARSE TM: fin = A_k + Q_l (lines 18-19)
-                if constexpr (TM && SPARSE) {
+                if constexpr (TM && (SPARSE || KC)) {
                     // short walks (B&B blocks): one TMEM round trip per couple,
                     // R_k and A_k reloaded only when k changes ((k, l) order)
                     uint32_t rl[NPLP], ql[NPLP];
@@ -1291,7 +1295,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                     for (int q = 0; q < NPL; ++q) ee[q] = (int)(ee[q] & 0xffff) - woff;
                 }
                 // lines 18-19: timeOnM2 = t1 + e with t1 = R_k + L_k at the end
-                if constexpr (TM && SPARSE) {
+                if constexpr (TM && (SPARSE || KC)) {
 #pragma unroll
                     for (int q = 0; q < NPL; ++q) lb[q] = max(lb[q], ee[q] + fin[q]);
                 } else if constexpr (TM) {
@@ -1366,6 +1370,14 @@ int launch(const fsp_lb_plan &pl, const LbArgs &a, cudaStream_t s)
             cudaError_t e = cudaGetLastError();
             return e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, "lb_kernel launch");
         }
+        if constexpr (!SPARSE) {
+            if (pl.kcache) {
+                lb_kernel<20, true, true, 4, false, true, false, true>
+                    <<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
+                cudaError_t e = cudaGetLastError();
+                return e == cudaSuccess ? FSP_OK : fsp_cuda_fail(e, "lb_kernel launch");
+            }
+        }
     }
     lb_kernel<MAXM, EXACT, S16, NPL, SPARSE, BYTE><<<pl.grid, pl.warps * 32, pl.smem_bytes, s>>>(a);
     cudaError_t e = cudaGetLastError();
@@ -1385,6 +1397,11 @@ int configure(fsp_lb_plan &pl)
         e = cudaFuncSetAttribute(lb_kernel<20, true, true, 4, SPARSE, true, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_optin);
         if (e != cudaSuccess) return fsp_cuda_fail(e, "cudaFuncSetAttribute");
+        if constexpr (!SPARSE) {
+            e = cudaFuncSetAttribute(lb_kernel<20, true, true, 4, false, true, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem_optin);
+            if (e != cudaSuccess) return fsp_cuda_fail(e, "cudaFuncSetAttribute");
+        }
     }
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel<MAXM, EXACT, S16, NPL, SPARSE, BYTE>,
@@ -1501,6 +1518,9 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                 (int64_t)((n + 1) / 2) * inst->max_p <= 65535;
         if (const char *s = getenv("FSP_LB_JP")) pl.jp = pl.jp && atoi(s) != 0;
     }
+    // R_k / A_k cached across couples in dense walks of short job lists (KC)
+    pl.kcache = !sparse && n <= 64;
+    if (const char *s = getenv("FSP_LB_KCACHE")) pl.kcache = !sparse && atoi(s) != 0;
     // Candidates: nodes per lane (4 only for the exact-m specialisations), warps
     // per CTA, fewest couple groups that fit.  Score = resident warps per SM
     // (latency hiding) x 1.5 for 4 nodes per lane (half the table and mask

@@ -514,3 +514,15 @@ def test_warp_per_node_mapping_flags_malformed(torch, fsp, monkeypatch):
     pf[9, 2] = n + 3  # job out of range
     gpu_lb(torch, inst, pf, dp)
     assert inst.check() == fsp.FSP_EBADNODE
+
+
+@pytest.mark.parametrize("name,kc", [("ta021", "0"), ("ta091", "1")])
+def test_parity_dense_kcache_switch(torch, fsp, orc, monkeypatch, name, kc):
+    """Dense 20-machine walks with R_k/A_k cached across couples (the default
+    for n <= 64) and without it (the default above) give the oracle's LBs
+    either way: each config run through its non-default variant."""
+    monkeypatch.setenv("FSP_LB_KCACHE", kc)
+    n, m, seed = inputs.TAILLARD_SEEDS[name]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, 3001, inputs.pool_seed(name) + 31)
+    compare(torch, fsp, orc, ptm, pf, dp)
