@@ -32,6 +32,16 @@
 #include "fsp_internal.h"
 
 
+// walk-loop unroll (x two 4-position steps per iteration), measured per
+// variant (profiles/r02/walk_unroll_ab.txt): 200x20 (dense, long lists) 8,
+// KC (n <= 64) 4, 5 machines 1; sparse (B&B) walks FSP_WALK_UNROLL_SPARSE
+#ifndef FSP_WALK_UNROLL_SPARSE
+#define FSP_WALK_UNROLL_SPARSE 1
+#endif
+#ifndef FSP_WALK_UNROLL_DENSE
+#define FSP_WALK_UNROLL_DENSE 8
+#endif
+
 namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -479,6 +489,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
     lb_kernel(const LbArgs a)
 {
     extern __shared__ __align__(128) uint8_t smem[];
+    constexpr int kUnroll = SPARSE ? FSP_WALK_UNROLL_SPARSE : MAXM <= 5 ? 1 : KC ? 4 : FSP_WALK_UNROLL_DENSE;
     if (a.pool_dev && *a.pool_dev == 0) return; // B&B: an empty (or rerouted) pool
     const int n = a.n;
     const int m = EXACT ? MAXM : a.m;
@@ -1264,6 +1275,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 Mask<MW> mx0 = FSP_MASK(xa.y), mx1 = FSP_MASK(xa.w);
                 Mask<MW> mx2 = FSP_MASK(xb.y), mx3 = FSP_MASK(xb.w);
                 int s = 0;
+#pragma unroll kUnroll
                 for (; s + 2 <= n4c; s += 2) {
                     const Mask<MW> my0 = FSP_MASK(ya.y), my1 = FSP_MASK(ya.w);
                     const Mask<MW> my2 = FSP_MASK(yb.y), my3 = FSP_MASK(yb.w);
