@@ -32,6 +32,10 @@
 #include "fsp_internal.h"
 
 
+// job-pair heads: two pairs per loop iteration (VIMNMX3 folds)
+#ifndef FSP_JP2
+#define FSP_JP2 1
+#endif
 // walk-loop unroll (x two 4-position steps per iteration), measured per
 // variant (profiles/r02/walk_unroll_ab.txt): 200x20 (dense, long lists) 8,
 // KC (n <= 64) 4, 5 machines 1; sparse (B&B) walks FSP_WALK_UNROLL_SPARSE
@@ -406,8 +410,70 @@ __device__ __forceinline__ bool jp_heads(const LbArgs &a, const uint32_t *s_jp, 
     const uint32_t *uw = Uw + useg + UL::word(lane, q);
     uint32_t cnt2 = 0;
     const int npair = (n + 1) >> 1; // row n of U is the always-empty padding row
+    int i = 0;
+#if FSP_JP2
+    // two pairs per iteration: their heads and tails fold into the minima with
+    // one 3-input VIMNMX3.U16x2 per machine (the forward pass does the heads
+    // and the loads, the backward pass reloads the rows for the tails)
+    auto flags = [&](int ip, uint32_t &ab, uint32_t &absw, uint32_t &M2) {
+        const uint32_t xl = uw[(2 * ip) * urow], xh = uw[(2 * ip + 1) * urow];
+        const uint32_t bl = (xl >> sh) & 1u, bh = (xh >> sh) & 1u;
+        ab = bl | (bh << 16);
+        absw = bh | (bl << 16);
+        M2 = MM - ab * M;
+    };
+    auto ldrow = [&](int ip, int k4) {
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"((uint32_t)__cvta_generic_to_shared(s_jp + (size_t)ip * MP4 + 4 * k4)));
+        return v;
+    };
 #pragma unroll 1
-    for (int i = 0; i < npair; ++i) {
+    for (; MAXM >= 10 && i + 1 < npair; i += 2) { // (5 machines: one pair at a time, measured)
+        uint32_t abA, abswA, M2A, abB, abswB, M2B;
+        flags(i, abA, abswA, M2A);
+        flags(i + 1, abB, abswB, M2B);
+        cnt2 += abA + abB;
+        uint32_t rA = __vmaxu2(C2[0], M2A), rB = __vmaxu2(C2[0], M2B);
+        RR[0] = __vimin3_u16x2(RR[0], rA, rB);
+#pragma unroll
+        for (int k4 = 0; k4 < MP4 / 4; ++k4) {
+            const uint4 va = ldrow(i, k4), vb = ldrow(i + 1, k4);
+            const uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int k = 4 * k4 + t;
+                if (k < MAXM) {
+                    LL[k] = wa[t] * abswA + LL[k];
+                    LL[k] = wb[t] * abswB + LL[k];
+                    if (k + 1 < MAXM) {
+                        rA = __viaddmax_u16x2(rA, wa[t], C2[k + 1]);
+                        rB = __viaddmax_u16x2(rB, wb[t], C2[k + 1]);
+                        RR[k + 1] = __vimin3_u16x2(RR[k + 1], rA, rB);
+                    }
+                }
+            }
+        }
+        uint32_t tA = M2A, tB = M2B;
+#pragma unroll
+        for (int k4 = MP4 / 4 - 1; k4 >= 0; --k4) {
+            const uint4 va = ldrow(i, k4), vb = ldrow(i + 1, k4);
+            const uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+            for (int t = 3; t >= 0; --t) {
+                const int k = 4 * k4 + t; // QQ[k-1] = min over jobs of q_j,k-1 + M2 = t after + p_jk
+                if (k >= 1 && k < MAXM) {
+                    tA = wa[t] * one + tA;
+                    tB = wb[t] * one + tB;
+                    QQ[k - 1] = __vimin3_u16x2(QQ[k - 1], tA, tB);
+                }
+            }
+        }
+    }
+#endif
+#pragma unroll 1
+    for (; i < npair; ++i) {
         const uint32_t xl = uw[(2 * i) * urow], xh = uw[(2 * i + 1) * urow];
         const uint32_t bl = (xl >> sh) & 1u, bh = (xh >> sh) & 1u;
         const uint32_t ab = bl | (bh << 16), absw = bh | (bl << 16);
