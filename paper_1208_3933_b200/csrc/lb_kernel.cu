@@ -1753,10 +1753,12 @@ int64_t fsp_lb_tail_first(const fsp_lb_plan &pl, int64_t pool)
 int fsp_lb_tail_split(const fsp_lb_plan &pl, int64_t pool, int split)
 {
     // measured on 200x20 1M pools: the idle warps of the partial wave were the
-    // whole 8 % "wait" share, but splitting their tiles (repeated phase A) did
-    // not shorten the launch (5.80 vs 5.82 ms): off unless FSP_LB_TAIL=1
+    // whole 8 % "wait" share; splitting their tiles (repeated phase A) did not
+    // shorten the round-2 launch (5.80 vs 5.82 ms), but with phase A at ~20 %
+    // it does (round 2b, profiles/r02/tail_split_ab.txt: 4.85 -> 4.80 ms,
+    // 50x20 1.384 -> 1.364): on unless FSP_LB_TAIL=0
     if (split != 1 || pool <= 0) return 1;
-    if (!getenv("FSP_LB_TAIL") || atoi(getenv("FSP_LB_TAIL")) == 0) return 1;
+    if (getenv("FSP_LB_TAIL") && atoi(getenv("FSP_LB_TAIL")) == 0) return 1;
     const int64_t tn = 32 * pl.npl, tiles = (pool + tn - 1) / tn;
     const int64_t slots = (int64_t)pl.grid * pl.warps;
     const int64_t rem = tiles - (fsp_lb_tail_first(pl, pool) / tn);
