@@ -32,6 +32,18 @@
 #include "fsp_internal.h"
 
 
+// node data read once per launch (depths, prefixes) as streaming loads
+// (evict-first), meant to keep the TMA ring's records in L2: measured off
+// (profiles/r02/stream_loads_ab.txt: DRAM reads 336 -> 384 MB per 200x20
+// launch, same time), so plain loads
+#ifndef FSP_STREAM_LOADS
+#define FSP_STREAM_LOADS 0
+#endif
+#if FSP_STREAM_LOADS
+#define FSP_LDS_STREAM(p) __ldcs(p)
+#else
+#define FSP_LDS_STREAM(p) (*(p))
+#endif
 // job-pair heads: two pairs per loop iteration (VIMNMX3 folds)
 #ifndef FSP_JP2
 #define FSP_JP2 1
@@ -710,7 +722,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
         for (int q = 0; q < NPL; ++q) {
             const long long node = tile * TN + q * 32 + lane;
             const bool has = node < pool;
-            int d = has ? a.depth[node] : 0;
+            int d = has ? FSP_LDS_STREAM(a.depth + node) : 0; // streamed: read once (evict-first)
             if (d < 0 || d > n || d > a.stride) {
                 bad = true;
                 d = 0;
@@ -788,7 +800,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 if (v16) {
                     const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
                     for (; i + 16 <= d; i += 16) { // two vectors in flight
-                        const uint4 v0 = r4[i >> 3], v1 = r4[(i >> 3) + 1];
+                        const uint4 v0 = FSP_LDS_STREAM(r4 + (i >> 3)), v1 = FSP_LDS_STREAM(r4 + (i >> 3) + 1);
                         const uint32_t w8[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
                         for (int t = 0; t < 8; ++t) {
@@ -1014,7 +1026,9 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
                     const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
                     for (; i + 8 <= dd; i += 8) {
-                        const uint4 v = r4[i >> 3];
+                        // streamed (evict-first): each prefix is read once, the couple
+                        // records the TMA ring re-reads stay in L2
+                        const uint4 v = FSP_LDS_STREAM(r4 + (i >> 3));
                         const uint32_t w8[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                         for (int t = 0; t < 8; ++t) st(t & 1 ? w8[t >> 1] >> 16 : w8[t >> 1] & 0xffffu);
