@@ -44,9 +44,13 @@
 #else
 #define FSP_LDS_STREAM(p) (*(p))
 #endif
-// job-pair heads: two pairs per loop iteration (VIMNMX3 folds)
+// job-pair heads: two pairs per loop iteration (VIMNMX3 folds); FSP_JP_SPLIT:
+// the tails in a second pass over the pairs
 #ifndef FSP_JP2
 #define FSP_JP2 1
+#endif
+#ifndef FSP_JP_SPLIT
+#define FSP_JP_SPLIT 0
 #endif
 // walk-loop unroll (x two 4-position steps per iteration), measured per
 // variant (profiles/r02/walk_unroll_ab.txt): 200x20 (dense, long lists) 8,
@@ -467,6 +471,7 @@ __device__ __forceinline__ bool jp_heads(const LbArgs &a, const uint32_t *s_jp, 
                 }
             }
         }
+#if !FSP_JP_SPLIT
         uint32_t tA = M2A, tB = M2B;
 #pragma unroll
         for (int k4 = MP4 / 4 - 1; k4 >= 0; --k4) {
@@ -482,7 +487,33 @@ __device__ __forceinline__ bool jp_heads(const LbArgs &a, const uint32_t *s_jp, 
                 }
             }
         }
+#endif
     }
+#if FSP_JP_SPLIT
+    // tails in a second pass over the pairs (fewer live registers per pass:
+    // no spills in either loop)
+#pragma unroll 1
+    for (int i2 = 0; MAXM >= 10 && i2 + 1 < npair; i2 += 2) {
+        uint32_t abA, abswA, M2A, abB, abswB, M2B;
+        flags(i2, abA, abswA, M2A);
+        flags(i2 + 1, abB, abswB, M2B);
+        uint32_t tA = M2A, tB = M2B;
+#pragma unroll
+        for (int k4 = MP4 / 4 - 1; k4 >= 0; --k4) {
+            const uint4 va = ldrow(i2, k4), vb = ldrow(i2 + 1, k4);
+            const uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+            for (int t = 3; t >= 0; --t) {
+                const int k = 4 * k4 + t;
+                if (k >= 1 && k < MAXM) {
+                    tA = wa[t] * one + tA;
+                    tB = wb[t] * one + tB;
+                    QQ[k - 1] = __vimin3_u16x2(QQ[k - 1], tA, tB);
+                }
+            }
+        }
+    }
+#endif
 #endif
 #pragma unroll 1
     for (; i < npair; ++i) {
