@@ -35,6 +35,13 @@ static inline int fsp_pq_words(int maxm) { return 2 * ((((maxm + 1) / 2) + 3) & 
 // u32 words per PTM row of the job-pair (jp) plans: 16-bit machine pairs
 // p_{j,2i} | p_{j,2i+1} << 16, padded to 16-byte rows.
 static inline int fsp_ptm16_words(int m) { return ((m + 1) / 2 + 3) & ~3; }
+// ... or, when every p_jk <= 255 (fsp_lb_plan::ptm8), 8-bit rows of 8-byte
+// units (one LDS.64 per 8 machines: half the C pass's gathered bytes again)
+static inline int fsp_ptm8_words(int m) { return 2 * ((m + 7) / 8); }
+static inline int fsp_ptm_row_words(bool jp, bool ptm8, int m)
+{
+    return !jp ? ((m + 3) & ~3) : ptm8 ? fsp_ptm8_words(m) : fsp_ptm16_words(m);
+}
 
 // Dynamic shared-memory layout of the lb kernel (byte offsets).
 struct fsp_lb_layout {
@@ -66,6 +73,7 @@ struct fsp_lb_plan {
     bool jp;             // dense TM plans: job-pair heads (PTM + job-pair rows staged, no pq
                          //   rows; lb_kernel.cu jp_heads), jp_m = the masking offset M
     int jp_m;
+    bool ptm8;           // jp plans with max p <= 255: 8-bit PTM rows for the C pass
     bool kcache;         // dense 20-machine walks: R_k, A_k cached while k is unchanged (n <= 64)
     bool recs_global;    // ablation: couple records read from global memory (20-machine dense)
     int warps;           // warps per CTA

@@ -96,13 +96,17 @@ static std::vector<int32_t> ptm_image(const int32_t *ptm, int n, int m, const fs
 {
     const int mp4 = (m + 3) & ~3;
     std::vector<int32_t> p32(pl.L.ptm_bytes / 4, 0);
-    if (pl.jp) { // 16-bit machine-pair rows for the C pass, then the job-pair rows
-        const int w16 = fsp_ptm16_words(m);
+    if (pl.jp) { // 16-bit (or 8-bit) rows for the C pass, then the job-pair rows
+        const int w16 = fsp_ptm_row_words(true, pl.ptm8, m);
         uint32_t *p16 = reinterpret_cast<uint32_t *>(p32.data());
         for (int j = 0; j < n; ++j)
-            for (int k = 0; k < m; ++k)
-                p16[(size_t)j * w16 + k / 2] |= (uint32_t)ptm[(size_t)j * m + k] << (16 * (k & 1));
-        uint32_t *jp = p16 + (size_t)n * w16;
+            for (int k = 0; k < m; ++k) {
+                if (pl.ptm8)
+                    p16[(size_t)j * w16 + k / 4] |= (uint32_t)ptm[(size_t)j * m + k] << (8 * (k & 3));
+                else
+                    p16[(size_t)j * w16 + k / 2] |= (uint32_t)ptm[(size_t)j * m + k] << (16 * (k & 1));
+            }
+        uint32_t *jp = p16 + (((size_t)n * w16 * 4 + 15) & ~size_t(15)) / 4; // 16-byte aligned block
         for (int j = 0; j < n; ++j)
             for (int k = 0; k < m; ++k)
                 jp[(size_t)(j / 2) * mp4 + k] |= (uint32_t)ptm[(size_t)j * m + k] << (16 * (j & 1));

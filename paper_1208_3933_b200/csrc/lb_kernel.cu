@@ -233,7 +233,9 @@ struct LbArgs {
     int sort_depth;        // fused dense path: the tile's nodes ranked by depth over the slots
     int jp;                // job-pair heads (fsp_lb_plan::jp): s_pq holds the job-pair rows
                            // and the C pass reads 16-bit PTM pair rows
-    int prow;              // u32 words per PTM row in shared memory (mp4, or m/2 padded to 4)
+    int prow;              // u32 words per PTM row in shared memory (fsp_ptm_row_words)
+    int ptm8;              // jp plans: 8-bit PTM rows (step8)
+    int jp_off;            // u32 words from PTM to the job-pair (or pq) rows
     uint32_t jp_m;         // their masking offset M (multiple of 16)
     uint32_t one;          // 1 (a multiplier ptxas keeps on the FMA pipe)
     int dbg_skip;          // diagnostics only (FSP_LB_DEBUG_SKIP): bit 0 skips the
@@ -614,7 +616,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
     // TM variants: per job [p pairs x HMP][q pairs x HMP] u32 after PTM (see fsp_plan_lb)
     // jp plans: PTM rows of packed 16-bit machine pairs (a.prow words), then the
     // job-pair rows; else int32 rows (mp4 words), then the (p, q) pair rows
-    const uint32_t *s_pq = reinterpret_cast<const uint32_t *>(s_ptm + (size_t)a.n * a.prow);
+    const uint32_t *s_pq = reinterpret_cast<const uint32_t *>(s_ptm + (size_t)a.jp_off);
     uint64_t *s_bar = reinterpret_cast<uint64_t *>(smem + a.L.off_bar);
     // per-warp heads R[MAXM][TN], A = R + L [MAXM][TN] (L_k = sum of p_jk over
     // the unscheduled jobs) and tails Q[MAXM][TN]; int16 in the s16 walk (all
@@ -1048,6 +1050,36 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                     else atomicAnd(&Uw[job * urow + useg + q], ~lanebit);
                 }
             };
+            // 8-bit rows (every p <= 255): one LDS.64 per 8 machines; each byte
+            // pair becomes the (p_k | p_k+1 << 16) word and its swap by PRMT
+            auto step8 = [&](uint32_t job) {
+                if (job >= (uint32_t)n) {
+                    bad = true;
+                    job = 0;
+                }
+                const uint2 *pr = reinterpret_cast<const uint2 *>(s_ptm + job * a.prow);
+                uint32_t prev = 0;
+#pragma unroll
+                for (int c8 = 0; c8 < (MAXM + 7) / 8; ++c8) {
+                    const uint2 v = pr[c8];
+                    const uint32_t w4[2] = {v.x, v.y};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) { // byte pairs (0,1) (2,3) of each word
+                        const int k = 8 * c8 + 2 * h;
+                        if (k < MAXM) {
+                            const uint32_t src = w4[h >> 1];
+                            const uint32_t w = __byte_perm(src, 0u, (h & 1) ? 0x4342u : 0x4140u);
+                            const uint32_t ws = __byte_perm(src, 0u, (h & 1) ? 0x4243u : 0x4041u);
+                            prev = __viaddmax_u16x2(prev, w, w * one + (uint32_t)C[k]);
+                            C[k] = (int)prev;
+                            if (k + 1 < MAXM) {
+                                prev = __viaddmax_u16x2(prev, ws, ws * one + (uint32_t)C[k + 1]);
+                                C[k + 1] = (int)prev;
+                            }
+                        }
+                    }
+                }
+            };
             // the prefix pass with step function ST (no branch between the jobs
             // of a vector: the scheduler overlaps consecutive jobs' chains)
             auto pass = [&](auto &&st) {
@@ -1073,10 +1105,17 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                     st(job);
                 }
             };
-            bool j16 = false;
-            if constexpr (!SPARSE && EXACT && S16) j16 = a.jp != 0;
-            if (j16) pass(step16);
-            else pass(step);
+            int jform = 0; // 0: int32 rows, 1: 16-bit rows, 2: 8-bit rows (5 machines only:
+                           // slower at 20 machines, profiles/r02/ptm8_ab.txt)
+            if constexpr (!SPARSE && EXACT && S16) jform = a.jp ? (a.ptm8 && MAXM <= 5 ? 2 : 1) : 0;
+            if constexpr (MAXM <= 5) {
+                if (jform == 2) pass(step8);
+                else if (jform == 1) pass(step16);
+                else pass(step);
+            } else {
+                if (jform == 1) pass(step16);
+                else pass(step);
+            }
             if (fused) __syncwarp(); // every lane's bits of node group q cleared
             // a2/a3: r_j0 = C_0, r_jk = max(C_k, r_j,k-1 + p_j,k-1) (R3); R_k =
             // min over unscheduled j (R5); Q_l = min_j q_jl, q_jl = sum_{i>l}
@@ -1641,6 +1680,9 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
                 (int64_t)((n + 1) / 2) * inst->max_p <= 65535;
         if (const char *s = getenv("FSP_LB_JP")) pl.jp = pl.jp && atoi(s) != 0;
     }
+    // 8-bit PTM rows for the jp plans' C pass when every p fits a byte
+    pl.ptm8 = pl.jp && inst->max_p <= 255 && m <= 5;
+    if (const char *s = getenv("FSP_LB_PTM8")) pl.ptm8 = pl.ptm8 && atoi(s) != 0;
     // R_k / A_k cached across couples in dense walks of short job lists (KC)
     pl.kcache = !sparse && n <= 64;
     if (const char *s = getenv("FSP_LB_KCACHE")) pl.kcache = !sparse && atoi(s) != 0;
@@ -1691,7 +1733,8 @@ int fsp_plan_lb(fsp_instance *inst, bool sparse)
             L.off_u = 0;
             // + the packed (p, q) machine-pair rows of the TM (nibble) variants
             // jp plans: + the job-pair rows [ceil(n/2)][mp4] (p_2i,k | p_2i+1,k << 16)
-            L.ptm_bytes = pl.jp ? (size_t)n * fsp_ptm16_words(m) * 4 + (size_t)((n + 1) / 2) * mp4 * 4
+            // (every TMA bulk copy is a multiple of 16 bytes: the row block is padded)
+            L.ptm_bytes = pl.jp ? align16((size_t)n * fsp_ptm_row_words(true, pl.ptm8, m) * 4) + (size_t)((n + 1) / 2) * mp4 * 4
                                 : align16((size_t)n * mp4 * 4) + (nib ? (size_t)n * fsp_pq_words(pl.maxm) * 4 : 0);
             L.off_ptm = L.u_bytes;
             L.off_bar = L.off_ptm + L.ptm_bytes;
@@ -1835,7 +1878,9 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.ptm = sparse ? inst->d_ptm32s_bb : inst->d_ptm32s;
     a.jp = pl.jp ? 1 : 0;
     a.sort_depth = getenv("FSP_LB_SORT") ? atoi(getenv("FSP_LB_SORT")) : 1;
-    a.prow = pl.jp ? fsp_ptm16_words(inst->m) : (inst->m + 3) & ~3;
+    a.prow = fsp_ptm_row_words(pl.jp, pl.ptm8, inst->m);
+    a.jp_off = (int)(align16((size_t)inst->n * a.prow * 4) / 4); // words to the jp / pq rows
+    a.ptm8 = pl.jp && pl.ptm8 ? 1 : 0;
     a.jp_m = (uint32_t)pl.jp_m;
     a.one = 1u;
     a.cin = cin;

@@ -278,6 +278,17 @@ def test_parity_heads_job_pairs_boundary(torch, fsp, orc, n, m):
 
 
 @pytest.mark.parametrize("name", ["ta001", "ta021", "ta091"])
+def test_c_pass_16bit_rows_ab(torch, fsp, orc, monkeypatch, name):
+    """Taillard times fit a byte, so the C pass reads 8-bit PTM rows by
+    default; FSP_LB_PTM8=0 forces the 16-bit rows: both match the oracle."""
+    monkeypatch.setenv("FSP_LB_PTM8", "0")
+    n, m, seed = inputs.TAILLARD_SEEDS[name]
+    ptm = inputs.taillard(n, m, seed)
+    pf, dp = inputs.pool_d1(n, 4000, inputs.pool_seed(name) + 6)
+    compare(torch, fsp, orc, ptm, pf, dp)
+
+
+@pytest.mark.parametrize("name", ["ta001", "ta021", "ta091"])
 def test_heads_job_pairs_ab(torch, fsp, orc, monkeypatch, name):
     """The same pool through the job-pair heads and the per-job heads
     (FSP_LB_JP=0, the A/B switch) gives identical LBs, equal to the oracle's."""
