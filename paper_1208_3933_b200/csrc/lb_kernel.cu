@@ -52,6 +52,10 @@
 #ifndef FSP_JP_SPLIT
 #define FSP_JP_SPLIT 0
 #endif
+// job-pair heads take the loads from the C pass (L = total - prefix sums)
+#ifndef FSP_JP_LC
+#define FSP_JP_LC 1
+#endif
 // walk-loop unroll (x two 4-position steps per iteration), measured per
 // variant (profiles/r02/walk_unroll_ab.txt): 200x20 (dense, long lists) 8,
 // KC (n <= 64) 4, 5 machines 1; sparse (B&B) walks FSP_WALK_UNROLL_SPARSE
@@ -236,6 +240,7 @@ struct LbArgs {
     int prow;              // u32 words per PTM row in shared memory (fsp_ptm_row_words)
     int ptm8;              // jp plans: 8-bit PTM rows (step8)
     int jp_off;            // u32 words from PTM to the job-pair (or pq) rows
+    uint32_t ltot2[16];    // per machine pair: sum_j p_j,2i | sum_j p_j,2i+1 << 16 (jp loads)
     uint32_t jp_m;         // their masking offset M (multiple of 16)
     uint32_t one;          // 1 (a multiplier ptxas keeps on the FMA pipe)
     int dbg_skip;          // diagnostics only (FSP_LB_DEBUG_SKIP): bit 0 skips the
@@ -410,10 +415,14 @@ __device__ __forceinline__ void warp_sort(uint32_t (&e)[NPL], int lane)
 
 // TM: R/A/Q to tensor memory as machine pairs (column (arr*HM + k/2)*NPLP + q);
 // else to the warp's shared arrays Rs/As/Qs [MAXM][TN] (16-bit), node q*32+lane.
-template <int MAXM, int HM, int NPLP, class UL, bool TM, int TN>
+// LC: the loads L_k come from the C pass (Lp = the prefix's machine-pair sums,
+// L = total - Lp) instead of one multiply-add per machine and job here (the
+// pools whose completion times are supplied, cin, have no C pass).
+template <int MAXM, int HM, int NPLP, class UL, bool TM, int TN, bool LC>
 __device__ __forceinline__ bool jp_heads(const LbArgs &a, const uint32_t *s_jp, const uint32_t *Uw,
                                          int urow, int useg, int lane, int q, const int (&C)[MAXM],
-                                         uint32_t tbase, uint16_t *Rs, int n, int want)
+                                         const uint32_t (&Lp)[HM], uint32_t tbase, uint16_t *Rs, int n,
+                                         int want)
 {
     constexpr int MP4 = (MAXM + 3) & ~3;
     uint32_t C2[MAXM], RR[MAXM], QQ[MAXM], LL[MAXM];
@@ -463,8 +472,10 @@ __device__ __forceinline__ bool jp_heads(const LbArgs &a, const uint32_t *s_jp, 
             for (int t = 0; t < 4; ++t) {
                 const int k = 4 * k4 + t;
                 if (k < MAXM) {
-                    LL[k] = wa[t] * abswA + LL[k];
-                    LL[k] = wb[t] * abswB + LL[k];
+                    if constexpr (!LC) {
+                        LL[k] = wa[t] * abswA + LL[k];
+                        LL[k] = wb[t] * abswB + LL[k];
+                    }
                     if (k + 1 < MAXM) {
                         rA = __viaddmax_u16x2(rA, wa[t], C2[k + 1]);
                         rB = __viaddmax_u16x2(rB, wb[t], C2[k + 1]);
@@ -547,10 +558,19 @@ __device__ __forceinline__ bool jp_heads(const LbArgs &a, const uint32_t *s_jp, 
             QQ[l] = __viaddmin_u16x2(t, pw[l + 1], QQ[l]);
             t = pw[l + 1] * one + t;
         }
+        if constexpr (!LC) {
 #pragma unroll
-        for (int k = 0; k < MAXM; ++k) LL[k] = pw[k] * absw + LL[k];
+            for (int k = 0; k < MAXM; ++k) LL[k] = pw[k] * absw + LL[k];
+        }
     }
     const int cnt = (int)((cnt2 & 0xffffu) + (cnt2 >> 16));
+    if constexpr (LC) { // L_k in the high halves, as the multiply-adds leave them
+#pragma unroll
+        for (int k = 0; k < MAXM; ++k) {
+            const uint32_t l2 = a.ltot2[k >> 1] - Lp[k >> 1]; // no borrow: every half total >= prefix
+            LL[k] = (k & 1) ? (l2 & 0xffff0000u) : (l2 << 16);
+        }
+    }
     if constexpr (!TM) {
         uint16_t *As = Rs + MAXM * TN, *Qs = As + MAXM * TN;
 #pragma unroll
@@ -1014,6 +1034,10 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
             // p_2i | p_2i+1 << 16; the chain runs in low halves (VIADDMNMX.U16x2,
             // the high halves collect garbage, masked off after the pass), odd
             // machines through a half swap
+            // jp plans: machine-pair sums of the prefix's p (the loads L = total - Lp)
+            uint32_t Lp[HM];
+#pragma unroll
+            for (int kp = 0; kp < HM; ++kp) Lp[kp] = 0u;
             auto step16 = [&](uint32_t job) {
                 if (job >= (uint32_t)n) {
                     bad = true;
@@ -1032,6 +1056,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                             const uint32_t w = w4[t], ws = __byte_perm(w, w, 0x1032);
                             prev = __viaddmax_u16x2(prev, w, w * one + (uint32_t)C[k]);
                             C[k] = (int)prev;
+                            Lp[k >> 1] = w * one + Lp[k >> 1];
                             if (k + 1 < MAXM) { // (odd m: the last machine has no pair)
                                 prev = __viaddmax_u16x2(prev, ws, ws * one + (uint32_t)C[k + 1]);
                                 C[k + 1] = (int)prev;
@@ -1072,6 +1097,7 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                             const uint32_t ws = __byte_perm(src, 0u, (h & 1) ? 0x4243u : 0x4041u);
                             prev = __viaddmax_u16x2(prev, w, w * one + (uint32_t)C[k]);
                             C[k] = (int)prev;
+                            Lp[k >> 1] = w * one + Lp[k >> 1];
                             if (k + 1 < MAXM) {
                                 prev = __viaddmax_u16x2(prev, ws, ws * one + (uint32_t)C[k + 1]);
                                 C[k + 1] = (int)prev;
@@ -1129,10 +1155,13 @@ __global__ void __launch_bounds__(MAXM > 20 ? 256 : MAXM <= 5 ? 128 : 512, MAXM 
                 if (a.jp) { // rows a2/a3 by job pairs (jp_heads), then the TMEM stores
 #pragma unroll
                     for (int k = 0; k < MAXM; ++k) C[k] &= 0xffff; // the 16-bit C pass's garbage
-                    if (jp_heads<MAXM, HM, NPLP, UL, TM, TN>(a, s_pq, Uw, urow, useg, lane, q, C, tbase,
-                                                             reinterpret_cast<uint16_t *>(Rs), n,
-                                                             node < pool ? n - d : 0))
-                        bad = true;
+                    const bool bd = (a.cin || !FSP_JP_LC || MAXM <= 5) ? jp_heads<MAXM, HM, NPLP, UL, TM, TN, false>(
+                                                a, s_pq, Uw, urow, useg, lane, q, C, Lp, tbase,
+                                                reinterpret_cast<uint16_t *>(Rs), n, node < pool ? n - d : 0)
+                                          : jp_heads<MAXM, HM, NPLP, UL, TM, TN, true>(
+                                                a, s_pq, Uw, urow, useg, lane, q, C, Lp, tbase,
+                                                reinterpret_cast<uint16_t *>(Rs), n, node < pool ? n - d : 0);
+                    if (bd) bad = true;
                     continue;
                 }
             }
@@ -1880,6 +1909,14 @@ int fsp_launch_lb_dev(const fsp_instance *inst, const uint16_t *prefix, int32_t 
     a.sort_depth = getenv("FSP_LB_SORT") ? atoi(getenv("FSP_LB_SORT")) : 1;
     a.prow = fsp_ptm_row_words(pl.jp, pl.ptm8, inst->m);
     a.jp_off = (int)(align16((size_t)inst->n * a.prow * 4) / 4); // words to the jp / pq rows
+    for (int kp = 0; kp < 16; ++kp) {
+        uint32_t lo = 0, hi = 0;
+        for (int j = 0; pl.jp && j < inst->n; ++j) {
+            if (2 * kp < inst->m) lo += (uint32_t)inst->h_ptm[(size_t)j * inst->m + 2 * kp];
+            if (2 * kp + 1 < inst->m) hi += (uint32_t)inst->h_ptm[(size_t)j * inst->m + 2 * kp + 1];
+        }
+        a.ltot2[kp] = lo | (hi << 16); // each sum <= n * max p < 2^16 (the 16-bit walk's condition)
+    }
     a.ptm8 = pl.jp && pl.ptm8 ? 1 : 0;
     a.jp_m = (uint32_t)pl.jp_m;
     a.one = 1u;
