@@ -63,4 +63,11 @@ h_dp = torch.from_numpy(dp).pin_memory()
 h_lb = torch.empty(len(dp), dtype=torch.int32).pin_memory()
 inst.lb_eval_host_ptr(h_pf.data_ptr(), pf.shape[1], h_dp.data_ptr(), len(dp), h_lb.data_ptr())
 print("host gather", int(h_lb.sum().item()), flush=True)
+# round 2b: the warp-per-sub-problem A/B kernel (wpn.cu)
+os.environ["FSP_LB_MAPPING"] = "warp"
+iw = binding.Instance(inputs.instance("ta021"))
+pf, dp = inputs.pool_d1(20, 301, 4)
+print("wpn", int(iw.lb_eval(torch.from_numpy(pf.view(np.int16)).cuda(), torch.from_numpy(dp).cuda()).sum().item()),
+      flush=True)
+os.environ.pop("FSP_LB_MAPPING")
 print("sanitize workload done")
