@@ -186,7 +186,8 @@ static int eval_host_gather(const fsp_instance *inst, HostCtx *c, const uint16_t
     {
         const int64_t q4 = (std::max<int64_t>(tile, chunk / 4) + tile - 1) / tile * tile;
         const int64_t q2 = (std::max<int64_t>(tile, chunk / 2) + tile - 1) / tile * tile;
-        const bool tail = ramp && getenv("FSP_HOST_TAIL") && pool >= 2 * (q4 + q2) + chunk;
+        const int tail_mode = getenv("FSP_HOST_TAIL") ? atoi(getenv("FSP_HOST_TAIL")) : 0;
+        const bool tail = ramp && tail_mode > 0 && pool >= 2 * (q4 + q2) + chunk;
         int64_t left = pool;
         std::vector<int64_t> head, mid, end;
         for (int64_t c : {q4, q2}) {
@@ -195,9 +196,9 @@ static int eval_host_gather(const fsp_instance *inst, HostCtx *c, const uint16_t
                 left -= head.back();
             }
         }
-        if (tail) {
-            end = {q2, q4};
-            left -= q2 + q4;
+        if (tail) { // 1: end on a half and a quarter wave; 2: on a half wave only
+            end = tail_mode == 2 ? std::vector<int64_t>{q2} : std::vector<int64_t>{q2, q4};
+            left -= tail_mode == 2 ? q2 : q2 + q4;
         }
         const int64_t full = left / chunk, rem = left - full * chunk;
         if (rem > 0 && tail) mid.push_back(rem);
