@@ -52,6 +52,10 @@
 #ifndef FSP_JP_SPLIT
 #define FSP_JP_SPLIT 0
 #endif
+// job-pair heads: byte-row flags by one PRMT (A/B switch)
+#ifndef FSP_JP_BYTEFLAGS
+#define FSP_JP_BYTEFLAGS 0 // measured: no difference (profiles/r02/jp_byteflags_ab.txt)
+#endif
 // job-pair heads take the loads from the C pass (L = total - prefix sums)
 #ifndef FSP_JP_LC
 #define FSP_JP_LC 1
@@ -443,10 +447,20 @@ __device__ __forceinline__ bool jp_heads(const LbArgs &a, const uint32_t *s_jp, 
     // one 3-input VIMNMX3.U16x2 per machine (the forward pass does the heads
     // and the loads, the backward pass reloads the rows for the tails)
     auto flags = [&](int ip, uint32_t &ab, uint32_t &absw, uint32_t &M2) {
-        const uint32_t xl = uw[(2 * ip) * urow], xh = uw[(2 * ip + 1) * urow];
-        const uint32_t bl = (xl >> sh) & 1u, bh = (xh >> sh) & 1u;
-        ab = bl | (bh << 16);
-        absw = bh | (bl << 16);
+        if constexpr (UL::BYTES && FSP_JP_BYTEFLAGS) {
+            // byte rows: the lane's two bytes, merged into one word by a PRMT, one
+            // shift and one mask give both flags at bits 0 and 16
+            const uint8_t *ub = reinterpret_cast<const uint8_t *>(Uw + useg) + lane;
+            const uint32_t w = __byte_perm((uint32_t)ub[(2 * ip) * urow * 4], (uint32_t)ub[(2 * ip + 1) * urow * 4],
+                                           0x1410u);
+            ab = (w >> (1 + q)) & 0x10001u;
+            absw = __byte_perm(ab, ab, 0x1032u);
+        } else {
+            const uint32_t xl = uw[(2 * ip) * urow], xh = uw[(2 * ip + 1) * urow];
+            const uint32_t bl = (xl >> sh) & 1u, bh = (xh >> sh) & 1u;
+            ab = bl | (bh << 16);
+            absw = bh | (bl << 16);
+        }
         M2 = MM - ab * M;
     };
     auto ldrow = [&](int ip, int k4) {
