@@ -14,6 +14,11 @@
 //     lists) or one word per 32 nodes (m = 5, int32 walk); each record carries
 //     the row's offset, so one multiply-add addresses a lane's mask;
 //   * per-node heads/tails (R, A = R + L, Q) live in tensor memory (TMEM);
+//   * phase A (completion times C_k, heads, tails, loads; rows a1-a3): the
+//     tile's nodes are dealt to the slots by depth rank (a warp bitonic sort),
+//     C_k comes from a 16-bit (5 machines: 8-bit) PTM-row pass that also sums
+//     the loads, the heads and tails run over job PAIRS in 16x2 ops with
+//     scheduled halves pushed above every real value (jp_heads, no branch);
 //   * the walk of Fig. 3 lines 08-17 is carried in the difference form
 //     e = timeOnM2 - timeOnM1:
 //         e <- max(e + x_j, y_j)      (if j unscheduled)
