@@ -981,7 +981,7 @@ int bb_create(const fsp_instance *inst, int32_t initial_ub, int32_t rank, int32_
     s->initial_inc = initial_ub == INT32_MAX ? INT32_MAX : initial_ub + 1; // R9
     s->sparse = getenv("FSP_BB_SPARSE") ? atoi(getenv("FSP_BB_SPARSE")) != 0 : true;
     // children per parent per pop: one lane per child in expand/order, K <= 32
-    s->K = (int)std::min<int64_t>(32, std::max<int64_t>(1, env_i64("FSP_BB_K", 8)));
+    s->K = (int)std::min<int64_t>(32, std::max<int64_t>(1, env_i64("FSP_BB_K", 12)));
     s->order = env_i64("FSP_BB_ORDER", 1) != 0 ? 1 : 0;
     // the beam: B*K*n <= beam * capacity.  A descent pushes at most B*K nodes
     // per level, and every iteration's B is also held to the free stack
